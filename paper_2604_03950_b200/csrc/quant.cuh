@@ -1,0 +1,338 @@
+// Phase 1 of the DMA forward: bit-exact dual MX quantization (paper Alg. 2).
+//
+// Restates quantize.py:122-212 on the GPU.  Every float64 operation that
+// feeds a rounding decision is performed in IEEE float64 in the reference's
+// order (x*c, gmax/2688, x_sm/S_q, bmax/6, blk/scale); the final f64 -> 8/4-bit
+// rounding goes through a round-to-odd f64 -> f32 step followed by the
+// hardware RNE-satfinite cvt, which is exact (no double rounding).  Two sign
+// fixups reproduce formats.py:144 (exact -0 -> +0 in E2M1) and
+// formats.py:240 (every zero magnitude -> +0 in FP8).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include "ptx.cuh"
+
+namespace dma {
+
+// ------------------------------------------------------------- scalar codecs
+__device__ __forceinline__ float rto_f32(double d) {
+  // round-to-odd float64 -> float32: truncate, then set the sticky LSB if inexact
+  float t = __double2float_rz(d);
+  if (static_cast<double>(t) != d) t = __uint_as_float(__float_as_uint(t) | 1u);
+  return t;
+}
+
+__device__ __forceinline__ int floor_log2_pos(double v) {
+  // exact floor(log2 v) for v > 0 (f64 subnormals give -1023, which every
+  // caller clamps to -127 exactly like np.maximum(v, tiny) in quantize.py:171)
+  return static_cast<int>((__double_as_longlong(v) >> 52) & 0x7FF) - 1023;
+}
+
+__device__ __forceinline__ double pow2(int e) {  // 2^e for e in [-1022, 1023]
+  return __hiloint2double((e + 1023) << 20, 0);
+}
+
+__device__ __forceinline__ double decode_e4m3(uint32_t c) {
+  uint32_t e = (c >> 3) & 0xF, m = c & 7;
+  double mag = e ? (8.0 + m) * pow2(static_cast<int>(e) - 10) : m * 0.001953125;  // 2^-9
+  return (c & 0x80) ? -mag : mag;
+}
+
+// E2M1 code of two values (each already clamped to [-6, 6]); returns (c1 << 4) | c0
+__device__ __forceinline__ uint32_t e2m1_pair(double v0, double v1) {
+  uint32_t mag = ptx::cvt_e2m1x2(fabsf(rto_f32(v0)), fabsf(rto_f32(v1)));
+  uint32_t s0 = (v0 < 0.0) ? 0x08u : 0u;  // exact -0.0 compares equal to 0 -> +0
+  uint32_t s1 = (v1 < 0.0) ? 0x80u : 0u;
+  return (mag | s0 | s1) & 0xFFu;
+}
+
+// FP8 codes of two values (clamped to the format range); byte0 = v0
+template <bool E5>
+__device__ __forceinline__ uint32_t fp8_pair(double v0, double v1) {
+  float a = fabsf(rto_f32(v0)), b = fabsf(rto_f32(v1));
+  uint32_t mag = E5 ? ptx::cvt_e5m2x2(a, b) : ptx::cvt_e4m3x2(a, b);
+  uint32_t c0 = mag & 0xFF, c1 = (mag >> 8) & 0xFF;
+  if (c0 && v0 < 0.0) c0 |= 0x80;  // rounded-to-zero magnitudes stay +0
+  if (c1 && v1 < 0.0) c1 |= 0x80;
+  return c0 | (c1 << 8);
+}
+
+__device__ __forceinline__ uint32_t e4m3_pos(double v) {  // code of a value > 0
+  uint32_t c = ptx::cvt_e4m3x2(rto_f32(v), 0.0f) & 0xFF;
+  return (c & 0x7F) ? c : 0u;
+}
+
+template <typename T>
+struct Load4;
+template <>
+struct Load4<double> {
+  __device__ static void run(const double* p, double (&v)[4]) {
+    double2 a = *reinterpret_cast<const double2*>(p);
+    double2 b = *reinterpret_cast<const double2*>(p + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+};
+template <>
+struct Load4<float> {
+  __device__ static void run(const float* p, double (&v)[4]) {
+    float4 a = *reinterpret_cast<const float4*>(p);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  }
+};
+template <>
+struct Load4<__nv_bfloat16> {
+  __device__ static void run(const __nv_bfloat16* p, double (&v)[4]) {
+    uint2 a = *reinterpret_cast<const uint2*>(p);
+    v[0] = __uint_as_float(a.x << 16);
+    v[1] = __uint_as_float(a.x & 0xFFFF0000u);
+    v[2] = __uint_as_float(a.y << 16);
+    v[3] = __uint_as_float(a.y & 0xFFFF0000u);
+  }
+};
+
+// Where phase 1 writes its results.  Canonical = the reference layout
+// (quantize.py:69-89); operand = what the phase-2 kernel loads (the element
+// arrays are shared: row-major K-major codes ARE the tcgen05 operand layout).
+struct QuantOut {
+  uint8_t* packed_low;   // [mat, rows, cols/2]
+  uint8_t* scales_low;   // [mat, rows, cols/V1]      canonical
+  uint8_t* high_codes;   // [mat, rows, cols]
+  uint8_t* scales_high;  // [mat, rows, cols/32]      canonical
+  double* quant_scale;   // [mat, rows] | [mat, rows, cols/32] | [mat]
+  uint8_t* sf_low_op;    // [mat, rtiles, chunks_low, 512]   tcgen05 scale-factor atoms
+  uint8_t* sf_high_op;   // [mat, rtiles, chunks_high, 512]
+  float* qs_f32;         // [mat, rows_pad] per-row S_q as f32 (TOKEN / TENSOR)
+  uint32_t* nonfinite;
+  int64_t rows_pad;      // rows rounded up to 128
+};
+
+// 32-row x 4-SF interleave of one 128-row scale-factor atom (cutlass
+// Sm1xxBlockScaledBasicChunk: offset (r%32)*16 + (r/32)*4 + k)
+__device__ __forceinline__ int64_t sf_atom_offset(int64_t mat, int64_t row, int kb, int64_t rtiles, int chunks) {
+  int r = static_cast<int>(row & 127);
+  int64_t tile = (mat * rtiles + (row >> 7)) * chunks + (kb >> 2);
+  return tile * 512 + (r & 31) * 16 + (r >> 5) * 4 + (kb & 3);
+}
+
+__device__ __forceinline__ double warp_max_xor(double v, int width_mask) {
+  for (int o = 1; o <= width_mask; o <<= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// One warp per row; lane l handles columns [128*ch + 4l, +4) for chunk ch.
+template <typename T, bool NV, bool E5, int GRAN>
+__global__ void __launch_bounds__(256) quant_rows_kernel(const T* __restrict__ x, int64_t n_mat, int64_t rows,
+                                                         int cols, int64_t mat_stride, int64_t row_stride,
+                                                         int is_query, double c,
+                                                         const unsigned long long* __restrict__ tensor_absmax,
+                                                         QuantOut out) {
+  constexpr int kMaxCh = 8;  // cols <= 1024
+  const int lane = threadIdx.x & 31;
+  const int64_t wrow = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wrow >= n_mat * rows) return;
+  const int64_t mat = wrow / rows, row = wrow % rows;
+  const T* xr = x + mat * mat_stride + row * row_stride;
+  const int nch = (cols + 127) >> 7;
+
+  double xs[kMaxCh][4];
+  double amax = 0.0;
+  bool bad = false;
+#pragma unroll
+  for (int ch = 0; ch < kMaxCh; ++ch) {
+    if (ch < nch) {
+      const int col0 = ch * 128 + lane * 4;
+      if (col0 < cols) {
+        Load4<T>::run(xr + col0, xs[ch]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          bad |= !isfinite(xs[ch][i]);
+          if (is_query) xs[ch][i] = __dmul_rn(xs[ch][i], c);  // quantize.py:149 (x * c)
+          amax = fmax(amax, fabs(xs[ch][i]));
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xs[ch][i] = 0.0;
+      }
+    }
+  }
+  if (out.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(out.nonfinite, 1u);
+
+  // ---- group max -> S_q (quantize.py:152-153)
+  double sq_row = 1.0;
+  if (GRAN == DMA_GRAN_TOKEN) {
+    double g = warp_max_xor(amax, 16);
+    sq_row = g > 0.0 ? __ddiv_rn(g, 2688.0) : 1.0;
+  } else if (GRAN == DMA_GRAN_TENSOR) {
+    double g = __longlong_as_double(static_cast<long long>(tensor_absmax[mat]));
+    if (is_query) g = __dmul_rn(g, c);  // max|x*c| == fl(max|x| * c): rounding is monotone
+    sq_row = g > 0.0 ? __ddiv_rn(g, 2688.0) : 1.0;
+  }
+  const int nsf_low = cols / (NV ? 16 : 32);
+  const int chunks_low = (nsf_low + 3) >> 2;
+  const int chunks_high = ((cols / 32) + 3) >> 2;
+  const int64_t rtiles = out.rows_pad >> 7;
+
+#pragma unroll
+  for (int ch = 0; ch < kMaxCh; ++ch) {
+    if (ch >= nch) break;
+    const int col0 = ch * 128 + lane * 4;
+    const bool valid = col0 < cols;  // warp-uniform per 8-lane group (cols % 32 == 0)
+    double sq = sq_row;
+    if (GRAN == DMA_GRAN_BLOCK) {
+      double m = fmax(fmax(fabs(xs[ch][0]), fabs(xs[ch][1])), fmax(fabs(xs[ch][2]), fabs(xs[ch][3])));
+      m = warp_max_xor(m, 4);
+      sq = m > 0.0 ? __ddiv_rn(m, 2688.0) : 1.0;
+    }
+    double xsc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) xsc[i] = __ddiv_rn(xs[ch][i], sq);  // quantize.py:154
+
+    // ---- 4-bit path (quantize.py:156-184)
+    double lv[4];
+    uint32_t sc_low;
+    if (NV) {
+      double bm = fmax(fmax(fabs(xsc[0]), fabs(xsc[1])), fmax(fabs(xsc[2]), fabs(xsc[3])));
+      bm = warp_max_xor(bm, 2);  // 16-column block = 4 lanes
+      uint32_t code = bm > 0.0 ? e4m3_pos(__ddiv_rn(bm, 6.0)) : 0x38u;
+      if (code == 0 && bm > 0.0) code = 0x01;  // floor at 2^-9 (quantize.py:164-167)
+      const double sv = decode_e4m3(code);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) lv[i] = fmin(fmax(__ddiv_rn(xsc[i], sv), -6.0), 6.0);
+      sc_low = code;
+    } else {
+      double bm = fmax(fmax(fabs(xs[ch][0]), fabs(xs[ch][1])), fmax(fabs(xs[ch][2]), fabs(xs[ch][3])));
+      bm = warp_max_xor(bm, 4);  // 32-column block = 8 lanes, single-level on x_sm
+      int e = bm > 0.0 ? min(max(floor_log2_pos(bm) - 2, -127), 127) : -127;
+      const double inv = pow2(-e);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) lv[i] = fmin(fmax(xs[ch][i] * inv, -6.0), 6.0);
+      sc_low = static_cast<uint32_t>(e + 127);
+    }
+    const uint32_t p01 = e2m1_pair(lv[0], lv[1]);
+    const uint32_t p23 = e2m1_pair(lv[2], lv[3]);
+
+    // ---- 8-bit path (quantize.py:186-199)
+    double hm = fmax(fmax(fabs(xsc[0]), fabs(xsc[1])), fmax(fabs(xsc[2]), fabs(xsc[3])));
+    hm = warp_max_xor(hm, 4);
+    constexpr int kEmax = E5 ? 15 : 8;
+    constexpr double kUpper = E5 ? 57344.0 : 448.0;
+    const int he = hm > 0.0 ? min(max(floor_log2_pos(hm) - kEmax, -127), 127) : -127;
+    const double hinv = pow2(-he);
+    double hv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) hv[i] = fmin(fmax(xsc[i] * hinv, -kUpper), kUpper);
+    const uint32_t c01 = fp8_pair<E5>(hv[0], hv[1]);
+    const uint32_t c23 = fp8_pair<E5>(hv[2], hv[3]);
+    const uint32_t sc_high = static_cast<uint32_t>(he + 127);
+
+    if (!valid) continue;
+    const int64_t rbase = mat * rows + row;
+    if (out.packed_low)
+      *reinterpret_cast<uint16_t*>(out.packed_low + rbase * (cols / 2) + col0 / 2) =
+          static_cast<uint16_t>(p01 | (p23 << 8));
+    if (out.high_codes)
+      *reinterpret_cast<uint32_t*>(out.high_codes + rbase * cols + col0) = c01 | (c23 << 16);
+    const bool low_leader = NV ? (lane & 3) == 0 : (lane & 7) == 0;
+    const int kb_low = col0 / (NV ? 16 : 32);
+    if (low_leader) {
+      if (out.scales_low) out.scales_low[rbase * nsf_low + kb_low] = static_cast<uint8_t>(sc_low);
+      if (out.sf_low_op)
+        out.sf_low_op[sf_atom_offset(mat, row, kb_low, rtiles, chunks_low)] = static_cast<uint8_t>(sc_low);
+    }
+    if ((lane & 7) == 0) {
+      const int kb = col0 / 32;
+      if (out.scales_high) out.scales_high[rbase * (cols / 32) + kb] = static_cast<uint8_t>(sc_high);
+      if (out.sf_high_op)
+        out.sf_high_op[sf_atom_offset(mat, row, kb, rtiles, chunks_high)] = static_cast<uint8_t>(sc_high);
+      if (GRAN == DMA_GRAN_BLOCK && out.quant_scale) out.quant_scale[rbase * (cols / 32) + kb] = sq;
+    }
+  }
+  if (lane == 0) {
+    if (GRAN == DMA_GRAN_TOKEN && out.quant_scale) out.quant_scale[mat * rows + row] = sq_row;
+    if (GRAN == DMA_GRAN_TENSOR && out.quant_scale && row == 0) out.quant_scale[mat] = sq_row;
+    if (GRAN != DMA_GRAN_BLOCK && out.qs_f32) out.qs_f32[mat * out.rows_pad + row] = static_cast<float>(sq_row);
+  }
+}
+
+// max |x| per matrix as the bit pattern of a non-negative double (atomicMax on u64)
+template <typename T>
+__global__ void __launch_bounds__(256) absmax_kernel(const T* __restrict__ x, int64_t rows, int cols,
+                                                     int64_t mat_stride, int64_t row_stride,
+                                                     unsigned long long* __restrict__ out) {
+  const int64_t mat = blockIdx.y;
+  const int64_t n = rows * cols;
+  double m = 0.0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, cc = i % cols;
+    double v;
+    if constexpr (sizeof(T) == 2) {
+      v = __bfloat162float(x[mat * mat_stride + r * row_stride + cc]);
+    } else {
+      v = static_cast<double>(x[mat * mat_stride + r * row_stride + cc]);
+    }
+    m = fmax(m, fabs(v));  // NaN inputs are reported separately through ``nonfinite``
+  }
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ double red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    atomicMax(out + mat, static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
+}
+
+// V -> MXFP8 (E4M3) along the key axis, for the block-scaled PV contraction.
+// One thread per (value column n, 32-key block).  Codes keep V's row-major
+// [keys, dv] layout (the MN-major B operand); the E8M0 scales go straight to
+// the tcgen05 atom layout with "row" = n and k-block = key block in the tile.
+// (No reference counterpart: the reference keeps V in float64, attention.py:250.)
+template <typename T>
+__global__ void __launch_bounds__(128) quant_v_kernel(const T* __restrict__ v, int64_t keys, int dv,
+                                                      int64_t keys_pad, uint8_t* __restrict__ codes,
+                                                      uint8_t* __restrict__ sf_op) {
+  const int n = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int64_t kblk = static_cast<int64_t>(blockIdx.y) * 4 + (threadIdx.x >> 5);
+  const int64_t mat = blockIdx.z;
+  if (n >= dv || kblk * 32 >= keys_pad) return;
+  const T* src = v + mat * keys * dv;
+  float vals[32];
+  float vmax = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int64_t key = kblk * 32 + i;
+    float f = 0.f;
+    if (key < keys) {
+      if constexpr (sizeof(T) == 2) f = __bfloat162float(src[key * dv + n]);
+      else f = static_cast<float>(src[key * dv + n]);
+    }
+    vals[i] = f;
+    vmax = fmaxf(vmax, fabsf(f));
+  }
+  int e = -127;
+  if (vmax > 0.f) {
+    const int fl = static_cast<int>((__float_as_uint(vmax) >> 23) & 0xFF) - 127;  // f32 subnormals -> -127
+    e = min(max(fl - 8, -127), 127);
+  }
+  const float inv = exp2f(static_cast<float>(-e));
+  uint8_t* dst = codes + mat * keys_pad * dv;
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {
+    const uint32_t pr = ptx::cvt_e4m3x2(vals[i] * inv, vals[i + 1] * inv);
+    const int64_t key = kblk * 32 + i;
+    dst[key * dv + n] = static_cast<uint8_t>(pr & 0xFF);
+    dst[(key + 1) * dv + n] = static_cast<uint8_t>(pr >> 8);
+  }
+  // scale atom: tile = key tile of 128, "row" = n, k-block = kblk % 4
+  const int64_t ktile = kblk >> 2;
+  const int64_t ntiles = keys_pad >> 7;
+  const int nchunk = (dv + 127) >> 7;  // dv <= 128 -> 1
+  const int64_t off = ((mat * ntiles + ktile) * nchunk + (n >> 7)) * 512 + ((n & 127) & 31) * 16 +
+                      ((n & 127) >> 5) * 4 + (kblk & 3);
+  sf_op[off] = static_cast<uint8_t>(e + 127);
+}
+
+}  // namespace dma
