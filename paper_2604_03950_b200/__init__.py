@@ -13,3 +13,8 @@ from .quantize import (  # noqa: F401
     QUANT_RANGE, DualQuantizedTensor, Granularity, dequantize_high, dequantize_low, quantize_dual,
     softmax_prescale,
 )
+from .attention import (  # noqa: F401
+    AttentionConfig, DmaAttention, causal_tile_plan, dma_attention, mixed_precision_attention,
+    noncausal_tile_plan,
+)
+from .metrics import MetricReport, high_precision_fraction, similarity  # noqa: F401

@@ -1,0 +1,185 @@
+"""DMA attention on the GPU (drop-in for ``mxattn.attention``).
+
+``mixed_precision_attention`` (alias ``dma_attention``) runs the fused
+sm_100a forward in libdma: phase 1 quantizes Q/K exactly like
+``quantize_dual`` (and V to MXFP8 along keys), phase 2 runs the
+diagonal-tiled attention with tcgen05 block-scaled MMAs following the same
+tile plans as the reference (attention.py:191-233).
+
+Differences from the float64 reference that are intrinsic to tensor cores
+(and covered by the stated tolerances in DESIGN.md / tests):
+  * scores accumulate in fp32 inside TMEM (the reference uses f64 dgemm);
+  * P and V enter the PV contraction as E4M3 x E8M0 (``pv_mode="mxfp8"``,
+    the default, block-scaled) or bf16 (``pv_mode="bf16"``, parity mode); the
+    reference keeps both in float64 (attention.py:174, 250).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._device import dtype_code, from_device, is_torch, to_device
+from .formats import MXFP8_E4M3, NVFP4, MxFormatSpec, format_code
+from .quantize import Granularity, granularity_code, prescale_constant
+
+_PV = {"mxfp8": _lib.PV_MXFP8, "bf16": _lib.PV_BF16}
+
+
+@dataclass(frozen=True)
+class AttentionConfig:
+    """attention.py:51-80 (same fields, defaults and validation), plus ``pv_mode``."""
+
+    tile_m: int = 64
+    tile_n: int = 64
+    diag_window: int = 0
+    sink_window: int = 0
+    causal: bool = True
+    low_format: MxFormatSpec | None = NVFP4
+    high_format: MxFormatSpec | None = MXFP8_E4M3
+    granularity: Granularity = Granularity.TOKEN
+    pv_mode: str = "mxfp8"
+
+    def __post_init__(self):
+        if self.tile_m < 1 or self.tile_n < 1:
+            raise ValueError("tile sizes must be >= 1")
+        if self.diag_window < 0 or self.sink_window < 0:
+            raise ValueError("window sizes must be >= 0")
+        if self.diag_window % self.tile_n or self.sink_window % self.tile_n:
+            raise ValueError(
+                "diag_window and sink_window must be multiples of tile_n "
+                f"(got {self.diag_window}/{self.sink_window} with tile_n={self.tile_n})")
+        if self.pv_mode not in _PV:
+            raise ValueError(f"pv_mode must be one of {sorted(_PV)}")
+
+
+# ---------------------------------------------------------------- tile plans
+def _plan(q_tile, len_q, len_k, cfg, causal):
+    buf = (ctypes.c_int64 * (2 + -(-max(len_k, 1) // cfg.tile_n)))()
+    n = _lib.lib().dma_tile_plan(q_tile, len_q, len_k, cfg.tile_m, cfg.tile_n, cfg.diag_window,
+                                 cfg.sink_window, int(causal), buf, len(buf))
+    return [(int(v) >> 1, bool(v & 1)) for v in buf[:n]]
+
+
+def causal_tile_plan(q_tile: int, len_q: int, len_k: int, cfg: AttentionConfig) -> list[tuple[int, bool]]:
+    """attention.py:191-209 (integer-exact; same code as the kernel's scheduler)."""
+    return _plan(q_tile, len_q, len_k, cfg, True)
+
+
+def noncausal_tile_plan(q_tile: int, len_q: int, len_k: int, cfg: AttentionConfig) -> list[tuple[int, bool]]:
+    """attention.py:212-233 (integer-exact; same code as the kernel's scheduler)."""
+    return _plan(q_tile, len_q, len_k, cfg, False)
+
+
+# ---------------------------------------------------------------- validation
+def _check_qkv(qs, ks, vs, causal):
+    """attention.py:109-119 on shapes [..., L, D]."""
+    if qs[-1] != ks[-1]:
+        raise ValueError(f"head dim mismatch: Q {tuple(qs)} vs K {tuple(ks)}")
+    if ks[-2] != vs[-2]:
+        raise ValueError(f"K/V row mismatch: {tuple(ks)} vs {tuple(vs)}")
+    if causal and qs[-2] != ks[-2]:
+        raise ValueError(f"causal attention requires equal sequence lengths, got {qs[-2]} and {ks[-2]}")
+
+
+def _args(cfg, q, k, v, o, B, H, KVH, Lq, Lk, D, DV, out_dtype):
+    a = _lib.DmaAttnArgs()
+    a.q, a.k, a.v, a.o = q.data_ptr(), k.data_ptr(), v.data_ptr(), (o.data_ptr() if o is not None else None)
+    a.in_dtype = dtype_code(q)
+    a.out_dtype = out_dtype
+    a.batch, a.heads, a.kv_heads, a.len_q, a.len_k, a.head_dim, a.v_dim = B, H, KVH, Lq, Lk, D, DV
+    a.tile_m, a.tile_n, a.diag_window, a.sink_window = cfg.tile_m, cfg.tile_n, cfg.diag_window, cfg.sink_window
+    a.causal = int(cfg.causal)
+    a.low_format = format_code(cfg.low_format)
+    a.high_format = format_code(cfg.high_format)
+    a.granularity = granularity_code(cfg.granularity)
+    a.pv_mode = _PV[cfg.pv_mode]
+    a.prescale = prescale_constant(D)
+    return a
+
+
+class DmaAttention:
+    """Reusable forward for fixed shapes: owns the phase-1 workspace.
+
+    q [B, H, Lq, D], k/v [B, KVH, Lk, D|DV] CUDA tensors (bf16/f32/f64).
+    """
+
+    def __init__(self, cfg: AttentionConfig):
+        self.cfg = cfg
+        self._ws = None
+
+    def workspace_for(self, a):
+        import torch
+
+        need = int(_lib.lib().dma_attention_workspace_bytes(a))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device="cuda")
+        return self._ws
+
+    def prepare(self, q, k, v, out=None, out_dtype=None):
+        import torch
+
+        B, H, Lq, D = q.shape
+        _, KVH, Lk, _ = k.shape
+        DV = v.shape[-1]
+        _check_qkv(q.shape, k.shape, v.shape, self.cfg.causal)
+        if (self.cfg.low_format or self.cfg.high_format) and D % 32:
+            raise ValueError(f"head dim {D} not divisible by 32")
+        if H % KVH:
+            raise ValueError(f"heads {H} not divisible by kv_heads {KVH}")
+        odt = out_dtype or (torch.bfloat16 if q.dtype == torch.bfloat16 else torch.float32)
+        if out is None:
+            out = torch.empty((B, H, Lq, DV), dtype=odt, device=q.device)
+        code = _lib.DT_BF16 if out.dtype == torch.bfloat16 else _lib.DT_F32
+        a = _args(self.cfg, q, k, v, out, B, H, KVH, Lq, Lk, D, DV, code)
+        rc = _lib.lib().dma_attention_supported(a)
+        _lib.check(rc, "dma_attention")
+        ws = self.workspace_for(a)
+        a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
+        return a, out
+
+    def __call__(self, q, k, v, out=None, out_dtype=None, stream=None):
+        a, out = self.prepare(q, k, v, out, out_dtype)
+        _lib.check(_lib.lib().dma_attention_fwd(a, _lib.stream_ptr(stream)), "dma_attention")
+        return out
+
+
+def dma_attention(q, k, v, cfg: AttentionConfig, out=None, out_dtype=None, stream=None):
+    """Batched forward on CUDA tensors [B, H, L, D] (also accepts [H, L, D] / [L, D])."""
+    nd = q.dim()
+    if nd not in (2, 3, 4):
+        raise ValueError("Q, K, V must be 2-D, 3-D or 4-D")
+    while q.dim() < 4:
+        q, k, v = q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0)
+    q, k, v = (to_device(t) for t in (q, k, v))
+    if not (q.dtype == k.dtype == v.dtype):
+        k, v = k.to(q.dtype), v.to(q.dtype)
+    o = DmaAttention(cfg)(q, k, v, out=out, out_dtype=out_dtype, stream=stream)
+    while o.dim() > nd:
+        o = o.squeeze(0)
+    return o
+
+
+def mixed_precision_attention(q, k, v, cfg: AttentionConfig):
+    """attention.py:282-310 on the GPU.  numpy in -> float64 numpy [Lq, Dv] out."""
+    if is_torch(q):
+        return dma_attention(q, k, v, cfg)
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    if q.ndim != 2 or k.ndim != 2 or v.ndim != 2:
+        raise ValueError("Q, K, V must be 2-D matrices")
+    _check_qkv(q.shape, k.shape, v.shape, cfg.causal)
+    if (cfg.low_format or cfg.high_format) and q.shape[1] % 32 != 0:
+        raise ValueError(f"head dim {q.shape[1]} not divisible by 32")
+    for x in (q, k):
+        if not np.all(np.isfinite(x)):
+            raise ValueError("quantize_dual: input contains non-finite values")
+    import torch
+
+    o = dma_attention(*(torch.from_numpy(np.ascontiguousarray(x)) for x in (q, k, v)), cfg,
+                      out_dtype=torch.float32)
+    return from_device(o).astype(np.float64)

@@ -1,13 +1,338 @@
-// C-ABI: the fused DMA forward (placeholder until the sm_100a kernel lands).
+// C-ABI: the DMA forward = phase 1 (quantize Q, K, V into the workspace in
+// tcgen05 operand layout) + phase 2 (dma_attn_kernel).  attention.py:282-310.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "attn.cuh"
 #include "common.cuh"
+#include "quant.cuh"
+
+namespace dma {
+
+int quantize_impl(const DmaQuantArgs* a, uint8_t* sf_low_op, uint8_t* sf_high_op, float* qs_f32, int64_t rows_pad,
+                  cudaStream_t st);
 
 static thread_local int g_launches = 0;
 
-extern "C" {
-size_t dma_attention_workspace_bytes(const DmaAttnArgs*) { return 0; }
-int dma_attention_supported(const DmaAttnArgs*) { return DMA_EUNSUPPORTED; }
-int dma_attention_quantize(const DmaAttnArgs*, void*) { return DMA_EUNSUPPORTED; }
-int dma_attention_core(const DmaAttnArgs*, void*) { return DMA_EUNSUPPORTED; }
-int dma_attention_fwd(const DmaAttnArgs*, void*) { return DMA_EUNSUPPORTED; }
-int dma_last_launch_count(void) { return g_launches; }
+// ------------------------------------------------------------ tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  });
+  return fn;
 }
+
+static CUtensorMapSwizzle swizzle_for(int row_bytes) {
+  return row_bytes >= 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+}
+
+// 3-D map over [mats][rows][inner] elements; box = [1][128][box_inner]
+static int make_map(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem_bytes, int64_t inner,
+                    int64_t rows, int64_t mats, int box_inner) {
+  EncodeTiledFn fn = encode_fn();
+  DMA_CHECK_ARG(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(mats)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(inner * elem_bytes), static_cast<cuuint64_t>(inner * rows * elem_bytes)};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(box_inner), 128u, 1u};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle_for(box_inner * elem_bytes), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): inner=%lld rows=%lld mats=%lld box=%d", (int)r, (long long)inner,
+              (long long)rows, (long long)mats, box_inner);
+    return DMA_EINVAL;
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------ workspace layout
+struct Layout {
+  int64_t mq, mk, lq_pad, lk_pad, ch_hi, ch_lo;
+  bool low_fp4, pv_bf16, v_convert, tensor_gran;
+  // byte offsets
+  size_t q_hi, q_lo, k_hi, k_lo, v_codes, v_bf16;  // large buffers
+  size_t small_begin, sf_q_hi, sf_q_lo, sf_k_hi, sf_k_lo, sf_v, qs_q, qs_k, small_end;
+  size_t absmax_q, absmax_k, total;
+};
+
+static size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static Layout plan_layout(const DmaAttnArgs* a) {
+  Layout L{};
+  L.mq = a->batch * a->heads;
+  L.mk = a->batch * a->kv_heads;
+  L.lq_pad = ceil_div(a->len_q, 128) * 128;
+  L.lk_pad = ceil_div(a->len_k, 128) * 128;
+  L.low_fp4 = (a->low_format == DMA_FMT_NVFP4 || a->low_format == DMA_FMT_MXFP4);
+  L.pv_bf16 = a->pv_mode == DMA_PV_BF16;
+  L.v_convert = L.pv_bf16 && a->in_dtype != DMA_DT_BF16;
+  L.tensor_gran = a->granularity == DMA_GRAN_TENSOR;
+  const int64_t D = a->head_dim, DV = a->v_dim;
+  L.ch_hi = (D / 32 + 3) / 4;
+  L.ch_lo = a->low_format == DMA_FMT_NVFP4 ? (D / 16 + 3) / 4 : (D / 32 + 3) / 4;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = up256(off + bytes);
+    return o;
+  };
+  L.q_hi = take(L.mq * a->len_q * D);
+  L.q_lo = L.low_fp4 ? take(L.mq * a->len_q * D / 2) : 0;
+  L.k_hi = take(L.mk * a->len_k * D);
+  L.k_lo = L.low_fp4 ? take(L.mk * a->len_k * D / 2) : 0;
+  L.v_codes = L.pv_bf16 ? 0 : take(L.mk * L.lk_pad * DV);
+  L.v_bf16 = L.v_convert ? take(L.mk * a->len_k * DV * 2) : 0;
+  L.small_begin = off;
+  L.sf_q_hi = take(L.mq * (L.lq_pad / 128) * L.ch_hi * 512);
+  L.sf_q_lo = L.low_fp4 ? take(L.mq * (L.lq_pad / 128) * L.ch_lo * 512) : 0;
+  L.sf_k_hi = take(L.mk * (L.lk_pad / 128) * L.ch_hi * 512);
+  L.sf_k_lo = L.low_fp4 ? take(L.mk * (L.lk_pad / 128) * L.ch_lo * 512) : 0;
+  L.sf_v = L.pv_bf16 ? 0 : take(L.mk * (L.lk_pad / 128) * ((DV + 127) / 128) * 512);
+  L.qs_q = take(L.mq * L.lq_pad * 4);
+  L.qs_k = take(L.mk * L.lk_pad * 4);
+  L.small_end = off;
+  L.absmax_q = L.tensor_gran ? take(L.mq * 8) : 0;
+  L.absmax_k = L.tensor_gran ? take(L.mk * 8) : 0;
+  L.total = off + 256;  // base alignment slack
+  return L;
+}
+
+static int validate(const DmaAttnArgs* a) {
+  DMA_CHECK_ARG(a != nullptr, "null args");
+  DMA_CHECK_ARG(a->batch >= 1 && a->heads >= 1 && a->kv_heads >= 1 && a->heads % a->kv_heads == 0,
+                "bad batch/heads/kv_heads (%lld/%lld/%lld)", (long long)a->batch, (long long)a->heads,
+                (long long)a->kv_heads);
+  DMA_CHECK_ARG(a->len_q >= 0 && a->len_k >= 0, "negative sequence length");
+  DMA_CHECK_ARG(!a->causal || a->len_q == a->len_k,
+                "causal attention requires equal sequence lengths, got %lld and %lld", (long long)a->len_q,
+                (long long)a->len_k);
+  DMA_CHECK_ARG(a->tile_m >= 1 && a->tile_n >= 1, "tile sizes must be >= 1");
+  DMA_CHECK_ARG(a->diag_window >= 0 && a->sink_window >= 0, "window sizes must be >= 0");
+  DMA_CHECK_ARG(a->diag_window % a->tile_n == 0 && a->sink_window % a->tile_n == 0,
+                "diag_window and sink_window must be multiples of tile_n");
+  DMA_CHECK_ARG(a->in_dtype >= DMA_DT_F64 && a->in_dtype <= DMA_DT_BF16, "bad in_dtype");
+  DMA_CHECK_ARG(a->out_dtype == DMA_DT_F32 || a->out_dtype == DMA_DT_BF16, "out_dtype must be f32 or bf16");
+  return 0;
+}
+
+int attention_supported(const DmaAttnArgs* a) {
+  if (int rc = validate(a)) return rc;
+  auto unsup = [](const char* why) {
+    set_error("%s", why);
+    return DMA_EUNSUPPORTED;
+  };
+  if (a->tile_m != 128 || a->tile_n != 128) return unsup("sm_100a kernel tiles are 128x128 (tile_m = tile_n = 128)");
+  if (a->head_dim != 64 && a->head_dim != 128) return unsup("head_dim must be 64 or 128");
+  if (a->v_dim != a->head_dim) return unsup("v_dim must equal head_dim");
+  if (a->high_format != DMA_FMT_MXFP8_E4M3 && a->high_format != DMA_FMT_MXFP8_E5M2)
+    return unsup("high_format must be an MXFP8 format (identity paths are not on the tensor-core kernel)");
+  if (a->low_format == DMA_FMT_NONE) return unsup("low_format=None (identity) is not on the tensor-core kernel");
+  if (a->granularity == DMA_GRAN_BLOCK) return unsup("BLOCK granularity is not on the tensor-core kernel yet");
+  if (a->pv_mode != DMA_PV_MXFP8 && a->pv_mode != DMA_PV_BF16) return unsup("bad pv_mode");
+  if (a->len_q > (int64_t(1) << 30) || a->len_k > (int64_t(1) << 30)) return unsup("sequence too long");
+  return 0;
+}
+
+__global__ void to_bf16_kernel(const void* src, int dt, int64_t n, __nv_bfloat16* dst) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float v = dt == DMA_DT_F64 ? static_cast<float>(static_cast<const double*>(src)[i])
+                               : static_cast<const float*>(src)[i];
+    dst[i] = __float2bfloat16_rn(v);
+  }
+}
+
+static int elem_bytes(int dt) { return dt == DMA_DT_F64 ? 8 : (dt == DMA_DT_F32 ? 4 : 2); }
+
+int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStream_t st) {
+  const int64_t D = a->head_dim, DV = a->v_dim;
+  const bool nv = a->low_format == DMA_FMT_NVFP4;
+  // padded SF atoms / S_q entries must be finite: zero the small region once per call
+  DMA_CUDA_TRY(cudaMemsetAsync(ws + L.small_begin, 0, L.small_end - L.small_begin, st));
+  ++g_launches;
+  for (int which = 0; which < 2; ++which) {
+    const bool isq = which == 0;
+    DmaQuantArgs q{};
+    q.x = isq ? a->q : a->k;
+    q.x_dtype = a->in_dtype;
+    q.is_query = isq;
+    q.n_mat = isq ? L.mq : L.mk;
+    q.rows = isq ? a->len_q : a->len_k;
+    q.cols = D;
+    q.mat_stride = q.rows * D;
+    q.row_stride = D;
+    q.prescale = a->prescale;
+    q.low_format = L.low_fp4 ? a->low_format : DMA_FMT_NVFP4;
+    q.high_format = a->high_format;
+    q.granularity = a->granularity;
+    q.packed_low = L.low_fp4 ? ws + (isq ? L.q_lo : L.k_lo) : nullptr;
+    q.high_codes = ws + (isq ? L.q_hi : L.k_hi);
+    q.workspace = L.tensor_gran ? ws + (isq ? L.absmax_q : L.absmax_k) : nullptr;
+    q.workspace_bytes = L.tensor_gran ? q.n_mat * 8 : 0;
+    uint8_t* sfl = L.low_fp4 ? ws + (isq ? L.sf_q_lo : L.sf_k_lo) : nullptr;
+    uint8_t* sfh = ws + (isq ? L.sf_q_hi : L.sf_k_hi);
+    float* qs = reinterpret_cast<float*>(ws + (isq ? L.qs_q : L.qs_k));
+    if (q.rows == 0) continue;
+    if (int rc = quantize_impl(&q, sfl, sfh, qs, isq ? L.lq_pad : L.lk_pad, st)) return rc;
+    g_launches += L.tensor_gran ? 2 : 1;
+  }
+  (void)nv;
+  if (a->len_k > 0) {
+    if (!L.pv_bf16) {
+      dim3 grid(static_cast<unsigned>((DV + 31) / 32), static_cast<unsigned>(L.lk_pad / 128),
+                static_cast<unsigned>(L.mk));
+      cudaStream_t s = st;
+      if (a->in_dtype == DMA_DT_BF16)
+        quant_v_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>(static_cast<const __nv_bfloat16*>(a->v), a->len_k,
+                                                           static_cast<int>(DV), L.lk_pad, ws + L.v_codes, ws + L.sf_v);
+      else if (a->in_dtype == DMA_DT_F32)
+        quant_v_kernel<float><<<grid, 128, 0, s>>>(static_cast<const float*>(a->v), a->len_k, static_cast<int>(DV),
+                                                   L.lk_pad, ws + L.v_codes, ws + L.sf_v);
+      else
+        quant_v_kernel<double><<<grid, 128, 0, s>>>(static_cast<const double*>(a->v), a->len_k,
+                                                    static_cast<int>(DV), L.lk_pad, ws + L.v_codes, ws + L.sf_v);
+      DMA_LAUNCH_CHECK();
+      ++g_launches;
+    } else if (L.v_convert) {
+      const int64_t n = L.mk * a->len_k * DV;
+      int64_t g = (n + 255) / 256;
+      g = g > 4096 ? 4096 : g;
+      to_bf16_kernel<<<static_cast<unsigned>(g), 256, 0, st>>>(a->v, a->in_dtype, n,
+                                                               reinterpret_cast<__nv_bfloat16*>(ws + L.v_bf16));
+      DMA_LAUNCH_CHECK();
+      ++g_launches;
+    }
+  }
+  return 0;
+}
+
+template <int D, int LOW, bool PVBF16>
+static int launch_attn(const AttnParams& p, int64_t items, cudaStream_t st) {
+  using C = AttnCfg<D, D, LOW, PVBF16>;
+  auto kern = dma_attn_kernel<D, D, LOW, PVBF16>;
+  const int smem = C::kSmemBytes > 120 * 1024 ? C::kSmemBytes : 120 * 1024;  // one CTA per SM (TMEM 512 cols)
+  DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<static_cast<unsigned>(items), 256, smem, st>>>(p);
+  DMA_LAUNCH_CHECK();
+  ++g_launches;
+  return 0;
+}
+
+template <int D>
+static int dispatch_attn(const AttnParams& p, int low, bool pv_bf16, int64_t items, cudaStream_t st) {
+  if (low == kLowNV) return pv_bf16 ? launch_attn<D, kLowNV, true>(p, items, st) : launch_attn<D, kLowNV, false>(p, items, st);
+  if (low == kLowMX4) return pv_bf16 ? launch_attn<D, kLowMX4, true>(p, items, st) : launch_attn<D, kLowMX4, false>(p, items, st);
+  return pv_bf16 ? launch_attn<D, kLowHigh, true>(p, items, st) : launch_attn<D, kLowHigh, false>(p, items, st);
+}
+
+int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStream_t st) {
+  const int64_t D = a->head_dim, DV = a->v_dim;
+  AttnParams p;
+  std::memset(&p, 0, sizeof(p));
+  const int64_t lq_rows = a->len_q > 0 ? a->len_q : 1, lk_rows = a->len_k > 0 ? a->len_k : 1;
+  if (int rc = make_map(&p.tm_q_hi, ws + L.q_hi, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, lq_rows, L.mq, (int)D)) return rc;
+  if (int rc = make_map(&p.tm_k_hi, ws + L.k_hi, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, lk_rows, L.mk, (int)D)) return rc;
+  if (L.low_fp4) {
+    if (int rc = make_map(&p.tm_q_lo, ws + L.q_lo, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D / 2, lq_rows, L.mq, (int)D / 2)) return rc;
+    if (int rc = make_map(&p.tm_k_lo, ws + L.k_lo, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D / 2, lk_rows, L.mk, (int)D / 2)) return rc;
+  }
+  if (L.pv_bf16) {
+    const void* vsrc = L.v_convert ? static_cast<const void*>(ws + L.v_bf16) : a->v;
+    DMA_CHECK_ARG((reinterpret_cast<uintptr_t>(vsrc) & 15) == 0, "V must be 16-byte aligned");
+    if (int rc = make_map(&p.tm_v, vsrc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, DV, lk_rows, L.mk, 64)) return rc;
+  } else {
+    if (int rc = make_map(&p.tm_v, ws + L.v_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, DV, L.lk_pad, L.mk, (int)DV)) return rc;
+  }
+  p.sf_q_hi = ws + L.sf_q_hi;
+  p.sf_q_lo = L.low_fp4 ? ws + L.sf_q_lo : nullptr;
+  p.sf_k_hi = ws + L.sf_k_hi;
+  p.sf_k_lo = L.low_fp4 ? ws + L.sf_k_lo : nullptr;
+  p.sf_v = L.pv_bf16 ? nullptr : ws + L.sf_v;
+  p.qs_q = reinterpret_cast<const float*>(ws + L.qs_q);
+  p.qs_k = reinterpret_cast<const float*>(ws + L.qs_k);
+  p.o = a->o;
+  p.out_bf16 = a->out_dtype == DMA_DT_BF16;
+  p.heads = static_cast<int>(a->heads);
+  p.kv_heads = static_cast<int>(a->kv_heads);
+  p.group = static_cast<int>(a->heads / a->kv_heads);
+  p.lq = static_cast<int>(a->len_q);
+  p.lk = static_cast<int>(a->len_k);
+  p.lq_pad = static_cast<int>(L.lq_pad);
+  p.lk_pad = static_cast<int>(L.lk_pad);
+  p.n_qt = static_cast<int>(L.lq_pad / 128);
+  p.diag_window = a->diag_window;
+  p.sink_window = a->sink_window;
+  p.causal = a->causal;
+  p.ch_hi = static_cast<int>(L.ch_hi);
+  p.ch_lo = static_cast<int>(L.ch_lo);
+  p.hfmt = a->high_format == DMA_FMT_MXFP8_E5M2 ? 1 : 0;
+  const int64_t items = L.mq * p.n_qt;
+  if (items == 0) return 0;
+  const int low = a->low_format == DMA_FMT_NVFP4 ? kLowNV : (a->low_format == DMA_FMT_MXFP4 ? kLowMX4 : kLowHigh);
+  return D == 64 ? dispatch_attn<64>(p, low, L.pv_bf16, items, st) : dispatch_attn<128>(p, low, L.pv_bf16, items, st);
+}
+
+static uint8_t* ws_base(const DmaAttnArgs* a) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(a->workspace) + 255) & ~uintptr_t(255));
+}
+
+}  // namespace dma
+
+using namespace dma;
+
+extern "C" {
+
+size_t dma_attention_workspace_bytes(const DmaAttnArgs* a) {
+  if (validate(a)) return 0;
+  return plan_layout(a).total;
+}
+
+int dma_attention_supported(const DmaAttnArgs* a) { return attention_supported(a); }
+
+int dma_attention_quantize(const DmaAttnArgs* a, void* stream) {
+  if (int rc = attention_supported(a)) return rc;
+  Layout L = plan_layout(a);
+  DMA_CHECK_ARG(a->workspace && a->workspace_bytes >= L.total, "workspace too small (%zu < %zu)",
+                a->workspace_bytes, L.total);
+  return attention_quantize(a, L, ws_base(a), static_cast<cudaStream_t>(stream));
+}
+
+int dma_attention_core(const DmaAttnArgs* a, void* stream) {
+  if (int rc = attention_supported(a)) return rc;
+  Layout L = plan_layout(a);
+  DMA_CHECK_ARG(a->workspace && a->workspace_bytes >= L.total, "workspace too small (%zu < %zu)",
+                a->workspace_bytes, L.total);
+  DMA_CHECK_ARG(a->o != nullptr, "null output");
+  return attention_core(a, L, ws_base(a), static_cast<cudaStream_t>(stream));
+}
+
+int dma_attention_fwd(const DmaAttnArgs* a, void* stream) {
+  g_launches = 0;
+  if (int rc = attention_supported(a)) return rc;
+  Layout L = plan_layout(a);
+  DMA_CHECK_ARG(a->workspace && a->workspace_bytes >= L.total, "workspace too small (%zu < %zu)",
+                a->workspace_bytes, L.total);
+  DMA_CHECK_ARG(a->q && a->k && a->v && a->o, "null tensor pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = attention_quantize(a, L, ws_base(a), st)) return rc;
+  return attention_core(a, L, ws_base(a), st);
+}
+
+int dma_last_launch_count(void) { return g_launches; }
+
+}  // extern "C"

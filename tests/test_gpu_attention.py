@@ -1,0 +1,120 @@
+"""GPU: DMA forward parity with the CPU oracle (same AttentionConfig, same inputs).
+
+Tolerances (stated per PV mode):
+  pv_mode="bf16"  (P, V in bf16; scores fp32)      rel-L2 <= 5e-3, max-abs <= 2e-2
+  pv_mode="mxfp8" (P -> E4M3 x2^8, V -> MXFP8/keys) rel-L2 <= 6e-2, max-abs <= 0.35
+Both are measured against the oracle's emulated-MX result
+(``mixed_precision_attention`` of the reference, restated in oracle/).
+"""
+
+import numpy as np
+import pytest
+
+from inputs import randn_bf16
+from oracle import mx_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"bf16": (5e-3, 2e-2), "mxfp8": (6e-2, 0.35)}
+
+
+def D():
+    import paper_2604_03950_b200 as m
+
+    return m
+
+
+def cfgs(low, high, gran, T, S, causal, pv):
+    d = D()
+    lo = {"nvfp4": (d.NVFP4, O.NVFP4), "mxfp4": (d.MXFP4, O.MXFP4), "mxfp8": (d.MXFP8_E4M3, O.MXFP8_E4M3)}[low]
+    hi = {"e4m3": (d.MXFP8_E4M3, O.MXFP8_E4M3), "e5m2": (d.MXFP8_E5M2, O.MXFP8_E5M2)}[high]
+    g = {"token": (d.Granularity.TOKEN, "token"), "tensor": (d.Granularity.TENSOR, "tensor")}[gran]
+    c = d.AttentionConfig(tile_m=128, tile_n=128, diag_window=T, sink_window=S, causal=causal,
+                          low_format=lo[0], high_format=hi[0], granularity=g[0], pv_mode=pv)
+    o = O.Cfg(tile_m=128, tile_n=128, diag_window=T, sink_window=S, causal=causal, low_format=lo[1],
+              high_format=hi[1], granularity=g[1])
+    return c, o
+
+
+def errs(got, want):
+    diff = got - want
+    return float(np.linalg.norm(diff) / np.linalg.norm(want)), float(np.abs(diff).max())
+
+
+CASES = [
+    # name, Lq, Lk, d, low, high, gran, T, S, causal
+    ("c1_n1024_d64_mxfp4", 1024, 1024, 64, "mxfp4", "e4m3", "token", 128, 128, True),
+    ("n1024_d128_nvfp4", 1024, 1024, 128, "nvfp4", "e4m3", "token", 128, 128, True),
+    ("n640_d128_mxfp4_T0", 640, 640, 128, "mxfp4", "e4m3", "token", 0, 0, True),
+    ("ragged_1000_d128_nvfp4", 1000, 1000, 128, "nvfp4", "e4m3", "token", 256, 128, True),
+    ("ragged_200_d64", 200, 200, 64, "nvfp4", "e4m3", "token", 128, 0, True),
+    ("noncausal_384x700_d128", 384, 700, 128, "nvfp4", "e4m3", "token", 256, 128, False),
+    ("noncausal_256x1024_d64_mx4", 256, 1024, 64, "mxfp4", "e4m3", "token", 128, 128, False),
+    ("low8_512_d128", 512, 512, 128, "mxfp8", "e4m3", "token", 0, 0, True),
+    ("e5m2_512_d128", 512, 512, 128, "nvfp4", "e5m2", "token", 128, 128, True),
+    ("tensor_768_d128", 768, 768, 128, "nvfp4", "e4m3", "tensor", 128, 128, True),
+    ("tensor_512_d64_mx4", 512, 512, 64, "mxfp4", "e4m3", "tensor", 0, 128, True),
+]
+
+
+@pytest.mark.parametrize("pv", ["bf16", "mxfp8"])
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_attention_vs_oracle(case, pv):
+    name, lq, lk, d, low, high, gran, T, S, causal = case
+    c, oc = cfgs(low, high, gran, T, S, causal, pv)
+    seed = abs(hash(name)) % 1000
+    q, k, v = randn_bf16(seed, lq, d), randn_bf16(seed + 1, lk, d), randn_bf16(seed + 2, lk, d)
+    got = D().mixed_precision_attention(q, k, v, c)
+    want = O.mixed_precision_attention(q, k, v, oc)
+    assert got.shape == want.shape and got.dtype == np.float64
+    rel, mx = errs(got, want)
+    print(f"{name} pv={pv}: rel_l2={rel:.3e} max_abs={mx:.3e}")
+    rtol, atol = TOL[pv]
+    assert np.isfinite(got).all()
+    assert rel <= rtol and mx <= atol, (rel, mx)
+
+
+@pytest.mark.parametrize("pv", ["bf16", "mxfp8"])
+def test_gqa_batched_torch(pv):
+    """c2-shaped GQA (H=8, KVH=2) batched 4-D bf16 path vs per-head oracle."""
+    import torch
+
+    B, H, KVH, N, d = 2, 8, 2, 512, 128
+    c, oc = cfgs("mxfp4", "e4m3", "token", 128, 128, True, pv)
+    g = torch.Generator().manual_seed(3)
+    q = torch.randn(B, H, N, d, generator=g).to(torch.bfloat16)
+    k = torch.randn(B, KVH, N, d, generator=g).to(torch.bfloat16)
+    v = torch.randn(B, KVH, N, d, generator=g).to(torch.bfloat16)
+    out = D().dma_attention(q.cuda(), k.cuda(), v.cuda(), c, out_dtype=torch.float32)
+    assert out.shape == (B, H, N, d)
+    out = out.cpu().double().numpy()
+    for b in range(B):
+        for h in (0, 3, 5, 7):
+            kh = h // (H // KVH)
+            want = O.mixed_precision_attention(q[b, h].double().numpy(), k[b, kh].double().numpy(),
+                                               v[b, kh].double().numpy(), oc)
+            rel, mx = errs(out[b, h], want)
+            assert rel <= TOL[pv][0] and mx <= TOL[pv][1], (b, h, rel, mx)
+
+
+def test_deterministic_and_bf16_out():
+    import torch
+
+    c, _ = cfgs("nvfp4", "e4m3", "token", 128, 128, True, "mxfp8")
+    g = torch.Generator().manual_seed(5)
+    q, k, v = (torch.randn(1, 4, 1024, 128, generator=g).to(torch.bfloat16).cuda() for _ in range(3))
+    a = D().dma_attention(q, k, v, c)
+    b = D().dma_attention(q, k, v, c)
+    assert a.dtype == torch.bfloat16
+    assert torch.equal(a, b)
+
+
+def test_unsupported_configs_raise():
+    d = D()
+    q = randn_bf16(1, 256, 64)
+    with pytest.raises(d._lib.DmaUnsupported):
+        d.mixed_precision_attention(q, q, q, d.AttentionConfig())  # 64-tiles
+    with pytest.raises(d._lib.DmaUnsupported):
+        d.mixed_precision_attention(q, q, q, d.AttentionConfig(tile_m=128, tile_n=128, low_format=None))
+    with pytest.raises(ValueError, match="causal"):
+        d.mixed_precision_attention(q, q[:128], q[:128], d.AttentionConfig(tile_m=128, tile_n=128))
