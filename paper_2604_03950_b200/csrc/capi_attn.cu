@@ -305,6 +305,7 @@ size_t dma_attention_workspace_bytes(const DmaAttnArgs* a) {
 int dma_attention_supported(const DmaAttnArgs* a) { return attention_supported(a); }
 
 int dma_attention_quantize(const DmaAttnArgs* a, void* stream) {
+  g_launches = 0;
   if (int rc = attention_supported(a)) return rc;
   Layout L = plan_layout(a);
   DMA_CHECK_ARG(a->workspace && a->workspace_bytes >= L.total, "workspace too small (%zu < %zu)",
