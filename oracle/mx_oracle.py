@@ -428,9 +428,51 @@ def operands(q, k, v, cfg):
     return ql, qh, kl, kh, v
 
 
-def mixed_precision_attention(q, k, v, cfg: Cfg) -> np.ndarray:
-    """Tile loop + base-2 online softmax (attention.py:150-175, 178-184, 282-310)."""
+def quantize_v_keys(v: np.ndarray) -> np.ndarray:
+    """Dequantized MXFP8 (E4M3) V with one E8M0 scale per 32 keys per column.
+
+    NOT part of the reference (which keeps V in float64, attention.py:250):
+    this is the block-scaled PV operand the north star asks for, restated so
+    tests can check the kernel against "reference algorithm + the kernel's
+    stated PV quantization".  The exponent rule is the reference's MXFP8 rule
+    (quantize.py:186-199, e = floor_log2(block max) - e_max, clip to +-448,
+    RNE) applied along the key axis with no S_q level.
+    """
+    v = np.asarray(v, dtype=np.float64)
+    n, dv = v.shape
+    pad = -n % 32
+    vp = np.concatenate([v, np.zeros((pad, dv))]) if pad else v
+    blk = vp.reshape(-1, 32, dv)
+    e = _pow2_exponent(np.abs(blk).max(axis=1), E4M3.e_max)[:, None, :]
+    hv = np.clip(blk * np.exp2(-e.astype(np.float64)), -E4M3.upper, E4M3.upper)
+    deq = decode_fp8(encode_fp8(hv, E4M3), E4M3) * np.exp2(e.astype(np.float64))
+    return deq.reshape(-1, dv)[:n]
+
+
+def _quantize_p(p: np.ndarray, pv: str) -> np.ndarray:
+    """P as the kernel feeds it to the PV contraction: E4M3(P * 2^8) * 2^-8, or bf16 (RNE)."""
+    if pv == "mxfp8":
+        return decode_fp8(encode_fp8(p * 256.0, E4M3), E4M3) / 256.0
+    if pv == "bf16":
+        b = p.astype(np.float32).view(np.uint32).astype(np.uint64)
+        b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+        return b.astype(np.uint32).view(np.float32).astype(np.float64)
+    return p
+
+
+def mixed_precision_attention(q, k, v, cfg: Cfg, pv: str = "f64") -> np.ndarray:
+    """Tile loop + base-2 online softmax (attention.py:150-175, 178-184, 282-310).
+
+    ``pv="f64"`` is the reference exactly.  ``pv="mxfp8"`` / ``"bf16"`` add the
+    sm_100a kernel's stated PV quantization (P -> E4M3 x 2^8 with V -> MXFP8
+    along keys, or P and V in bf16) on top of the same algorithm; the row sum
+    l still uses the unquantized P, as the kernel does.  Test infrastructure only.
+    """
     ql, qh, kl, kh, v = operands(q, k, v, cfg)
+    if pv == "mxfp8":
+        v = quantize_v_keys(v)
+    elif pv == "bf16":
+        v = _quantize_p(v, "bf16")
     lq, lk = ql.shape[0], kl.shape[0]
     tm, tn = cfg.tile_m, cfg.tile_n
     out = np.empty((lq, v.shape[1]))
@@ -453,7 +495,7 @@ def mixed_precision_attention(q, k, v, cfg: Cfg) -> np.ndarray:
             ok = np.isfinite(s)
             p[ok] = np.exp2((s - np.where(alive, m_new, 0.0)[:, None])[ok])
             l = l * alpha + p.sum(axis=1)
-            acc = acc * alpha[:, None] + p @ v[k0:k1]
+            acc = acc * alpha[:, None] + _quantize_p(p, pv) @ v[k0:k1]
             m = m_new
         out[q0:q1] = acc / np.where(l > 0, l, 1.0)[:, None]
     return out

@@ -194,18 +194,19 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
   (void)nv;
   if (a->len_k > 0) {
     if (!L.pv_bf16) {
-      dim3 grid(static_cast<unsigned>((DV + 31) / 32), static_cast<unsigned>(L.lk_pad / 128),
-                static_cast<unsigned>(L.mk));
+      // dv in {64, 128} (attention_supported): 256 threads = 256 / (dv/2) key blocks of 32
+      const int kb_per_cta = 256 / static_cast<int>(DV / 2);
+      dim3 grid(static_cast<unsigned>((L.lk_pad / 32 + kb_per_cta - 1) / kb_per_cta), static_cast<unsigned>(L.mk));
       cudaStream_t s = st;
       if (a->in_dtype == DMA_DT_BF16)
-        quant_v_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>(static_cast<const __nv_bfloat16*>(a->v), a->len_k,
-                                                           static_cast<int>(DV), L.lk_pad, ws + L.v_codes, ws + L.sf_v);
+        quant_v2_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(a->v), a->len_k,
+                                                            static_cast<int>(DV), L.lk_pad, ws + L.v_codes, ws + L.sf_v);
       else if (a->in_dtype == DMA_DT_F32)
-        quant_v_kernel<float><<<grid, 128, 0, s>>>(static_cast<const float*>(a->v), a->len_k, static_cast<int>(DV),
-                                                   L.lk_pad, ws + L.v_codes, ws + L.sf_v);
+        quant_v2_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(a->v), a->len_k, static_cast<int>(DV),
+                                                    L.lk_pad, ws + L.v_codes, ws + L.sf_v);
       else
-        quant_v_kernel<double><<<grid, 128, 0, s>>>(static_cast<const double*>(a->v), a->len_k,
-                                                    static_cast<int>(DV), L.lk_pad, ws + L.v_codes, ws + L.sf_v);
+        quant_v2_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double*>(a->v), a->len_k,
+                                                     static_cast<int>(DV), L.lk_pad, ws + L.v_codes, ws + L.sf_v);
       DMA_LAUNCH_CHECK();
       ++g_launches;
     } else if (L.v_convert) {

@@ -24,6 +24,15 @@ template <typename T, bool NV, bool E5, int GRAN>
 static void launch_rows(const DmaQuantArgs* a, const unsigned long long* tmax, const QuantOut& out,
                         cudaStream_t st) {
   const int64_t nrows = a->n_mat * a->rows;
+  const int64_t tpr = a->cols / 16;
+  if (tpr <= 32 && (tpr & (tpr - 1)) == 0 && a->row_stride % 8 == 0 && a->mat_stride % 8 == 0) {
+    // fast path: 16 columns per thread (cols in {32, 64, 128, 256, 512})
+    const int64_t blocks = (nrows * tpr + 255) / 256;
+    quant16_kernel<T, NV, E5, GRAN><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+        static_cast<const T*>(a->x), a->n_mat, a->rows, static_cast<int>(a->cols), a->mat_stride, a->row_stride,
+        a->is_query, a->prescale, tmax, out);
+    return;
+  }
   const int64_t blocks = (nrows + 7) / 8;
   quant_rows_kernel<T, NV, E5, GRAN><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
       static_cast<const T*>(a->x), a->n_mat, a->rows, static_cast<int>(a->cols), a->mat_stride, a->row_stride,

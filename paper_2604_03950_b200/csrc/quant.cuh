@@ -256,6 +256,225 @@ __global__ void __launch_bounds__(256) quant_rows_kernel(const T* __restrict__ x
   }
 }
 
+// ------------------------------------------------------------------------
+// Throughput variant (the one the forward path uses): one thread owns 16
+// consecutive columns of one row (exactly one NVFP4 block, half an MX
+// block), so a row of ``cols`` is ``tpr = cols/16`` adjacent lanes and every
+// group reduction is a short xor-shuffle.  Same decisions as
+// quant_rows_kernel, cheaper arithmetic:
+//   * a/b in float64 as q = a*y, r = fma(-q, b, a), q' = fma(r, y, q) with
+//     y = RN(1/b) (Markstein's theorem: q' == RN(a/b) for these operand
+//     ranges; 4e8 brute-force cases in DESIGN.md) -- one reciprocal per row /
+//     block instead of a full division per element;
+//   * round-to-odd f64 -> f32 on the bit pattern (integer pipe);
+//   * no clamps: cvt.rn.satfinite already saturates to +-6 / +-448 / +-57344
+//     exactly like the reference's clip-then-round (formats.py:133-134,220-224).
+// f64 inputs keep IEEE __ddiv_rn (their range is not bounded like bf16/f32).
+// ------------------------------------------------------------------------
+__device__ __forceinline__ double mk_div(double a, double b, double y) {
+  const double q = __dmul_rn(a, y);
+  const double r = __fma_rn(-q, b, a);
+  return __fma_rn(r, y, q);
+}
+
+// |v| rounded to odd as an f32 (0 for |v| < 2^-126: rounds to +-0 in every target format)
+__device__ __forceinline__ float rto_abs(double v) {
+  const uint32_t hi = static_cast<uint32_t>(__double2hiint(v)) & 0x7FFFFFFFu;
+  const uint32_t lo = static_cast<uint32_t>(__double2loint(v));
+  if (hi < 0x38100000u) return 0.0f;
+  uint32_t f = __funnelshift_l(lo, hi - 0x38000000u, 3);
+  f |= (lo & 0x1FFFFFFFu) != 0u ? 1u : 0u;
+  return __uint_as_float(f);
+}
+__device__ __forceinline__ bool neg_nonzero(double v) { return v < 0.0; }
+
+template <typename T>
+struct Load16;
+template <>
+struct Load16<__nv_bfloat16> {
+  __device__ static void run(const __nv_bfloat16* p, double (&v)[16]) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(p) + 1);
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+};
+template <>
+struct Load16<float> {
+  __device__ static void run(const float* p, double (&v)[16]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(p) + i);
+      v[4 * i] = a.x; v[4 * i + 1] = a.y; v[4 * i + 2] = a.z; v[4 * i + 3] = a.w;
+    }
+  }
+};
+template <>
+struct Load16<double> {
+  __device__ static void run(const double* p, double (&v)[16]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(p) + i);
+      v[2 * i] = a.x; v[2 * i + 1] = a.y;
+    }
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ double qdiv(double a, double b, double y) {
+  if constexpr (sizeof(T) == 8) return __ddiv_rn(a, b);
+  else return mk_div(a, b, y);
+}
+
+__device__ __forceinline__ double shfl_max(double v, int lanes) {
+  for (int o = 1; o < lanes; o <<= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <typename T, bool NV, bool E5, int GRAN>
+__global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, int64_t n_mat, int64_t rows,
+                                                      int cols, int64_t mat_stride, int64_t row_stride,
+                                                      int is_query, double c,
+                                                      const unsigned long long* __restrict__ tensor_absmax,
+                                                      QuantOut out) {
+  const int tpr = cols >> 4;  // power of two in [2, 32]
+  const int lane = threadIdx.x & 31;
+  const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t grow = gt / tpr;  // mat * rows + row
+  const int part = static_cast<int>(gt % tpr);
+  const bool live = grow < n_mat * rows;  // whole rows live or die together (tpr | 32)
+  if (__all_sync(0xffffffffu, !live)) return;
+  const int64_t mat = live ? grow / rows : 0, row = live ? grow % rows : 0;
+
+  double xs[16];
+  if (live) {
+    Load16<T>::run(x + mat * mat_stride + row * row_stride + part * 16, xs);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) xs[i] = 0.0;
+  }
+  bool bad = false;
+  double amax = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    bad |= (static_cast<uint32_t>(__double2hiint(xs[i])) & 0x7FF00000u) == 0x7FF00000u;  // Inf / NaN
+    if (is_query) xs[i] = __dmul_rn(xs[i], c);  // quantize.py:149 (x * c)
+    amax = fmax(amax, fabs(xs[i]));
+  }
+  if (out.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(out.nonfinite, 1u);
+
+  // ---- group max -> S_q (quantize.py:98-106, 152-153)
+  double g;
+  if (GRAN == DMA_GRAN_TOKEN) {
+    g = shfl_max(amax, tpr);
+  } else if (GRAN == DMA_GRAN_BLOCK) {
+    g = shfl_max(amax, 2);
+  } else {
+    g = __longlong_as_double(static_cast<long long>(tensor_absmax[mat]));
+    if (is_query) g = __dmul_rn(g, c);  // max|x*c| == fl(max|x| * c): rounding is monotone
+  }
+  const double sq = g > 0.0 ? __ddiv_rn(g, 2688.0) : 1.0;
+  const double ysq = __drcp_rn(sq);
+  double xsc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) xsc[i] = qdiv<T>(xs[i], sq, ysq);  // quantize.py:154
+
+  // ---- 4-bit path (quantize.py:156-184)
+  uint32_t packed[2] = {0u, 0u};
+  uint32_t sc_low;
+  if (NV) {
+    double bm = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) bm = fmax(bm, fabs(xsc[i]));
+    uint32_t code = bm > 0.0 ? e4m3_pos(__ddiv_rn(bm, 6.0)) : 0x38u;
+    if (code == 0 && bm > 0.0) code = 0x01;  // floor at 2^-9 (quantize.py:164-167)
+    const double sv = decode_e4m3(code);
+    const double ysv = __drcp_rn(sv);
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+      const double l0 = qdiv<T>(xsc[i], sv, ysv), l1 = qdiv<T>(xsc[i + 1], sv, ysv);
+      uint32_t b = ptx::cvt_e2m1x2(rto_abs(l0), rto_abs(l1));
+      b |= (neg_nonzero(l0) ? 0x08u : 0u) | (neg_nonzero(l1) ? 0x80u : 0u);
+      packed[i >> 3] |= b << (4 * (i & 7));
+    }
+    sc_low = code;
+  } else {
+    double bm = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) bm = fmax(bm, fabs(xs[i]));
+    bm = shfl_max(bm, 2);  // 32-column block = 2 lanes, single level on x_sm
+    const int e = bm > 0.0 ? min(max(floor_log2_pos(bm) - 2, -127), 127) : -127;
+    const double inv = pow2(-e);
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+      const double l0 = xs[i] * inv, l1 = xs[i + 1] * inv;
+      uint32_t b = ptx::cvt_e2m1x2(rto_abs(l0), rto_abs(l1));
+      b |= (neg_nonzero(l0) ? 0x08u : 0u) | (neg_nonzero(l1) ? 0x80u : 0u);
+      packed[i >> 3] |= b << (4 * (i & 7));
+    }
+    sc_low = static_cast<uint32_t>(e + 127);
+  }
+
+  // ---- 8-bit path (quantize.py:186-199)
+  double hm = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) hm = fmax(hm, fabs(xsc[i]));
+  hm = shfl_max(hm, 2);
+  constexpr int kEmax = E5 ? 15 : 8;
+  const int he = hm > 0.0 ? min(max(floor_log2_pos(hm) - kEmax, -127), 127) : -127;
+  const double hinv = pow2(-he);
+  uint32_t codes[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i += 2) {
+      const double h0 = xsc[4 * j + i] * hinv, h1 = xsc[4 * j + i + 1] * hinv;
+      const float a = rto_abs(h0), b = rto_abs(h1);
+      const uint32_t mag = E5 ? ptx::cvt_e5m2x2(a, b) : ptx::cvt_e4m3x2(a, b);
+      uint32_t c0 = mag & 0xFF, c1 = (mag >> 8) & 0xFF;
+      if (c0 && neg_nonzero(h0)) c0 |= 0x80;  // rounded-to-zero magnitudes stay +0
+      if (c1 && neg_nonzero(h1)) c1 |= 0x80;
+      w |= (c0 | (c1 << 8)) << (8 * i);
+    }
+    codes[j] = w;
+  }
+  const uint32_t sc_high = static_cast<uint32_t>(he + 127);
+  if (!live) return;
+
+  const int64_t rbase = mat * rows + row;
+  const int col0 = part * 16;
+  if (out.packed_low)
+    *reinterpret_cast<uint2*>(out.packed_low + rbase * (cols / 2) + col0 / 2) = make_uint2(packed[0], packed[1]);
+  if (out.high_codes)
+    *reinterpret_cast<uint4*>(out.high_codes + rbase * cols + col0) = make_uint4(codes[0], codes[1], codes[2], codes[3]);
+  const int nsf_low = cols / (NV ? 16 : 32);
+  const int chunks_low = (nsf_low + 3) >> 2;
+  const int chunks_high = ((cols / 32) + 3) >> 2;
+  const int64_t rtiles = out.rows_pad >> 7;
+  const bool even = (part & 1) == 0;
+  if (NV || even) {
+    const int kb_low = NV ? part : (part >> 1);
+    if (out.scales_low) out.scales_low[rbase * nsf_low + kb_low] = static_cast<uint8_t>(sc_low);
+    if (out.sf_low_op) out.sf_low_op[sf_atom_offset(mat, row, kb_low, rtiles, chunks_low)] = static_cast<uint8_t>(sc_low);
+  }
+  if (even) {
+    const int kb = part >> 1;
+    if (out.scales_high) out.scales_high[rbase * (cols / 32) + kb] = static_cast<uint8_t>(sc_high);
+    if (out.sf_high_op) out.sf_high_op[sf_atom_offset(mat, row, kb, rtiles, chunks_high)] = static_cast<uint8_t>(sc_high);
+    if (GRAN == DMA_GRAN_BLOCK && out.quant_scale) out.quant_scale[rbase * (cols / 32) + kb] = sq;
+  }
+  if (part == 0) {
+    if (GRAN == DMA_GRAN_TOKEN && out.quant_scale) out.quant_scale[rbase] = sq;
+    if (GRAN == DMA_GRAN_TENSOR && out.quant_scale && row == 0) out.quant_scale[mat] = sq;
+    if (GRAN != DMA_GRAN_BLOCK && out.qs_f32) out.qs_f32[mat * out.rows_pad + row] = static_cast<float>(sq);
+  }
+}
+
 // max |x| per matrix as the bit pattern of a non-negative double (atomicMax on u64)
 template <typename T>
 __global__ void __launch_bounds__(256) absmax_kernel(const T* __restrict__ x, int64_t rows, int cols,
@@ -333,6 +552,66 @@ __global__ void __launch_bounds__(128) quant_v_kernel(const T* __restrict__ v, i
   const int64_t off = ((mat * ntiles + ktile) * nchunk + (n >> 7)) * 512 + ((n & 127) & 31) * 16 +
                       ((n & 127) >> 5) * 4 + (kblk & 3);
   sf_op[off] = static_cast<uint8_t>(e + 127);
+}
+
+// V -> MXFP8 (E4M3) along keys, coalesced variant: a thread owns two adjacent
+// value columns of one 32-key block (4-byte loads, 2-byte code stores, a warp
+// covers 64 contiguous columns of a key row).  Same arithmetic as
+// quant_v_kernel.  blockDim = 256; a CTA covers 256 / (dv/2) key blocks.
+template <typename T>
+__global__ void __launch_bounds__(256) quant_v2_kernel(const T* __restrict__ v, int64_t keys, int dv,
+                                                       int64_t keys_pad, uint8_t* __restrict__ codes,
+                                                       uint8_t* __restrict__ sf_op) {
+  const int tpb = dv >> 1;                      // threads per key block
+  const int n = (threadIdx.x % tpb) * 2;        // first of my two columns
+  const int64_t kblk = static_cast<int64_t>(blockIdx.x) * (blockDim.x / tpb) + threadIdx.x / tpb;
+  const int64_t mat = blockIdx.y;
+  if (kblk * 32 >= keys_pad) return;
+  const T* src = v + mat * keys * dv + n;
+  float a[32], b[32];
+  float ma = 0.f, mb = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int64_t key = kblk * 32 + i;
+    float f0 = 0.f, f1 = 0.f;
+    if (key < keys) {
+      if constexpr (sizeof(T) == 2) {
+        const uint32_t w = __ldg(reinterpret_cast<const unsigned int*>(src + key * dv));
+        f0 = __uint_as_float(w << 16);
+        f1 = __uint_as_float(w & 0xFFFF0000u);
+      } else {
+        f0 = static_cast<float>(src[key * dv]);
+        f1 = static_cast<float>(src[key * dv + 1]);
+      }
+    }
+    a[i] = f0;
+    b[i] = f1;
+    ma = fmaxf(ma, fabsf(f0));
+    mb = fmaxf(mb, fabsf(f1));
+  }
+  auto expo = [](float m) {
+    if (!(m > 0.f)) return -127;
+    const int fl = static_cast<int>((__float_as_uint(m) >> 23) & 0xFF) - 127;  // f32 subnormals -> -127
+    return min(max(fl - 8, -127), 127);
+  };
+  const int ea = expo(ma), eb = expo(mb);
+  const float ia = exp2f(static_cast<float>(-ea)), ib = exp2f(static_cast<float>(-eb));
+  uint8_t* dst = codes + mat * keys_pad * dv + n;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const uint32_t pr = ptx::cvt_e4m3x2(a[i] * ia, b[i] * ib);
+    *reinterpret_cast<uint16_t*>(dst + (kblk * 32 + i) * dv) = static_cast<uint16_t>(pr);
+  }
+  const int64_t ktile = kblk >> 2;
+  const int64_t ntiles = keys_pad >> 7;
+  const int nchunk = (dv + 127) >> 7;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int c = n + j;
+    const int64_t off = ((mat * ntiles + ktile) * nchunk + (c >> 7)) * 512 + ((c & 127) & 31) * 16 +
+                        ((c & 127) >> 5) * 4 + (kblk & 3);
+    sf_op[off] = static_cast<uint8_t>((j ? eb : ea) + 127);
+  }
 }
 
 }  // namespace dma

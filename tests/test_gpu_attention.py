@@ -1,11 +1,21 @@
 """GPU: DMA forward parity with the CPU oracle (same AttentionConfig, same inputs).
 
-Tolerances (stated per PV mode):
-  pv_mode="bf16"  (P, V in bf16; scores fp32)      rel-L2 <= 5e-3, max-abs <= 2e-2
-  pv_mode="mxfp8" (P -> E4M3 x2^8, V -> MXFP8/keys) rel-L2 <= 6e-2, max-abs <= 0.35
-Both are measured against the oracle's emulated-MX result
-(``mixed_precision_attention`` of the reference, restated in oracle/).
+Two references, two tolerances per PV mode:
+
+* the oracle exactly (``mixed_precision_attention`` of the reference, restated
+  in oracle/; P and V stay float64 there, attention.py:174,250):
+    pv_mode="bf16"  (P, V in bf16; scores fp32)       rel-L2 <= 5e-3, max-abs <= 2e-2
+    pv_mode="mxfp8" (P -> E4M3 x2^8, V -> MXFP8/keys) rel-L2 <= 6e-2, max-abs <= 0.6
+  (max-abs under MXFP8 PV is dominated by the first causal rows, where one or
+  two quantized V rows carry the whole output: |v| ~ 4 x 2^-4 relative step);
+* the oracle with the kernel's stated PV quantization applied
+  (``pv="bf16"|"mxfp8"``), which isolates what the kernel itself adds
+  (fp32 TMEM accumulation, ex2.approx, E4M3 rounding flips of P):
+    both PV modes    rel-L2 <= 5e-4, max-abs <= 5e-3
+  (first B200 run: rel-L2 1e-7 .. 6e-5, max-abs <= 6.3e-4 over these cases)
 """
+
+import zlib
 
 import numpy as np
 import pytest
@@ -15,7 +25,8 @@ from oracle import mx_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"bf16": (5e-3, 2e-2), "mxfp8": (6e-2, 0.35)}
+TOL = {"bf16": (5e-3, 2e-2), "mxfp8": (6e-2, 0.6)}
+TOL_EMU = {"bf16": (5e-4, 5e-3), "mxfp8": (5e-4, 5e-3)}
 
 
 def D():
@@ -62,16 +73,19 @@ CASES = [
 def test_attention_vs_oracle(case, pv):
     name, lq, lk, d, low, high, gran, T, S, causal = case
     c, oc = cfgs(low, high, gran, T, S, causal, pv)
-    seed = abs(hash(name)) % 1000
+    seed = zlib.crc32(name.encode()) % 1000
     q, k, v = randn_bf16(seed, lq, d), randn_bf16(seed + 1, lk, d), randn_bf16(seed + 2, lk, d)
     got = D().mixed_precision_attention(q, k, v, c)
     want = O.mixed_precision_attention(q, k, v, oc)
     assert got.shape == want.shape and got.dtype == np.float64
+    emu = O.mixed_precision_attention(q, k, v, oc, pv=pv)
     rel, mx = errs(got, want)
-    print(f"{name} pv={pv}: rel_l2={rel:.3e} max_abs={mx:.3e}")
-    rtol, atol = TOL[pv]
+    erel, emx = errs(got, emu)
+    print(f"{name} pv={pv}: vs oracle rel_l2={rel:.3e} max_abs={mx:.3e}; "
+          f"vs oracle+PV emulation rel_l2={erel:.3e} max_abs={emx:.3e}")
     assert np.isfinite(got).all()
-    assert rel <= rtol and mx <= atol, (rel, mx)
+    assert erel <= TOL_EMU[pv][0] and emx <= TOL_EMU[pv][1], (erel, emx)
+    assert rel <= TOL[pv][0] and mx <= TOL[pv][1], (rel, mx)
 
 
 @pytest.mark.parametrize("pv", ["bf16", "mxfp8"])
