@@ -6,19 +6,31 @@
 // attention.py:150-175 (l0 = 0, dead rows keep alpha = 1, normalisation
 // guard l > 0 from attention.py:104-106).
 //
-// One CTA = one (batch, head, 128-row query tile).  Warp roles:
-//   warp 0      TMA producer: Q (hi+lo codes, SF atoms) once, then per plan
-//               entry the K tile in the entry's precision (+SF, +S_q^K) into
-//               a 3-stage ring and the V tile into a 2-stage ring
+// Persistent kernel: one CTA per SM walks the work items (batch, head,
+// 128-row query tile) in longest-first order (causal cost grows with the
+// query tile), CTA c taking items c, c + grid, c + 2 grid, ...  Consecutive
+// items share the query tile and differ in head, so co-resident CTAs of one
+// GQA group read the same K/V tiles through L2.
+//
+// Warp roles (384 threads):
+//   warp 0      TMA producer: Q (hi + lo codes, SF atoms) per item into a
+//               2-deep ring, then per plan entry the K tile in the entry's
+//               precision (+ SF + S_q^K) into a kNK ring and V (+ SF) into a
+//               kNV ring
 //   warp 1      MMA issuer (one thread): S = Q K^T (kind::mxf8f6f4 for high
-//               tiles, kind::mxf4nvf4 4X / kind::mxf4 2X for low tiles) into a
-//               double-buffered S in TMEM; O += P V (kind::mxf8f6f4 with P
-//               read from TMEM, or kind::f16 in the bf16 parity mode)
-//   warps 4-7   softmax: one query row per thread; S_q^Q x S_q^K rescale,
-//               causal / ragged mask, online max/sum, exp2, P -> E4M3 (x2^8)
-//               or bf16 written back into the S columns in TMEM, O rescale,
-//               final O / l epilogue
-// TMEM (512 cols): S0 [0,128) S1 [128,256) O [256,256+DV) scale factors [384,424)
+//               tiles, kind::mxf4nvf4 4X / kind::mxf4 2X for low tiles) into
+//               a double-buffered S in TMEM, one tile of look-ahead (also
+//               across items); O += P V (kind::mxf8f6f4 with P read from TMEM,
+//               or kind::f16 in the bf16 parity mode)
+//   warps 4-7   softmax half 0: key columns [0, 64) of every S tile
+//   warps 8-11  softmax half 1: key columns [64, 128)
+//               Thread (half g, quadrant q, lane l) owns query row 32q + l.
+//               Per tile: S_q^Q x S_q^K rescale, causal / ragged mask, row max
+//               (exchanged with the partner half through shared memory), exp2,
+//               P -> E4M3 (x 2^8) or bf16 written back into its own S columns
+//               in TMEM, row sum, O rescale of its half of the O columns;
+//               epilogue O / l of its O columns.
+// TMEM (512 cols): S0 [0,128) S1 [128,256) O [256,256+DV) scale factors [384,436)
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -44,7 +56,7 @@ struct __align__(64) AttnParams {
   int out_bf16;
   int heads, kv_heads, group;  // group = heads / kv_heads
   int lq, lk, lq_pad, lk_pad;
-  int n_qt;
+  int n_qt, n_bh, n_items;
   int diag_window, sink_window, causal;
   int ch_hi, ch_lo;
   int hfmt;  // high-path element format: 0 = E4M3, 1 = E5M2
@@ -53,33 +65,37 @@ struct __align__(64) AttnParams {
 template <int D, int DV, int LOW, bool PVBF16>
 struct AttnCfg {
   static constexpr int kBM = 128, kBN = 128;
-  static constexpr int kNK = 3, kNV = 2;
+  static constexpr int kNQ = 2, kNK = 4, kNV = 3;
   static constexpr int kQHiBytes = kBM * D;
   static constexpr int kQLoBytes = kBM * D / 2;
+  static constexpr int kQStage = ((kQHiBytes + (LOW != kLowHigh ? kQLoBytes : 0) + 1023) / 1024) * 1024;
   static constexpr int kKBytes = kBN * D;  // fp8 size; fp4 tiles use half
   static constexpr int kVBytes = PVBF16 ? kBN * DV * 2 : kBN * DV;
   static constexpr int kChHi = (D / 32 + 3) / 4;
   static constexpr int kChLo = LOW == kLowNV ? (D / 16 + 3) / 4 : (D / 32 + 3) / 4;
   static constexpr int kChK = kChHi > kChLo ? kChHi : kChLo;
   // smem carve-up (offsets from a 1024-aligned base)
-  static constexpr int oQHi = 0;
-  static constexpr int oQLo = oQHi + kQHiBytes;
-  static constexpr int oK = ((oQLo + kQLoBytes + 1023) / 1024) * 1024;
-  static constexpr int kKStage = kKBytes;
-  static constexpr int oV = oK + kNK * kKStage;
+  static constexpr int oQ = 0;
+  static constexpr int oK = oQ + kNQ * kQStage;
+  static constexpr int oV = oK + kNK * kKBytes;
   static constexpr int oSmall = oV + kNV * kVBytes;
-  static constexpr int oSfQHi = oSmall;
-  static constexpr int oSfQLo = oSfQHi + 512 * kChHi;
-  static constexpr int oSfK = oSfQLo + 512 * kChLo;
-  static constexpr int oSqK = oSfK + kNK * 512 * kChK;
-  static constexpr int oSfV = oSqK + kNK * 512;
-  static constexpr int oSfP = oSfV + kNV * 512;
-  static constexpr int oBar = oSfP + 512;
-  static constexpr int kSmemBytes = oBar + 256 + 1024;  // + alignment slack
+  static constexpr int oSfQ = oSmall;                        // [kNQ][kChHi + kChLo][512]
+  static constexpr int kSfQStage = 512 * (kChHi + kChLo);
+  static constexpr int oSfK = oSfQ + kNQ * kSfQStage;        // [kNK][kChK][512]
+  static constexpr int oSqK = oSfK + kNK * 512 * kChK;       // [kNK][128] f32
+  static constexpr int oSfV = oSqK + kNK * 512;              // [kNV][512]
+  static constexpr int oSfP = oSfV + kNV * 512;              // 512
+  static constexpr int oRed = oSfP + 512;                    // [2 buf][2 half][128] f32 row maxima
+  static constexpr int oRedL = oRed + 2 * 2 * 128 * 4;       // [2 half][128] f32 row sums
+  static constexpr int oBar = oRedL + 2 * 128 * 4;
+  static constexpr int kSmemBytes = oBar + 256 + 1024;       // + alignment slack
   // TMEM columns
   static constexpr uint32_t tS0 = 0, tS1 = 128, tO = 256;
-  static constexpr uint32_t tSfQHi = 384, tSfQLo = 388, tSfK0 = 396, tSfK1 = 404, tSfV0 = 412, tSfV1 = 416,
-                            tSfP = 420;
+  static constexpr uint32_t tSfQ = 384;  // [kNQ][hi 4 | lo 8] = 24 cols
+  static constexpr uint32_t tSfK = 408;  // [2][8]
+  static constexpr uint32_t tSfV = 424;  // [2][4]
+  static constexpr uint32_t tSfP = 432;  // 4
+  static_assert(tSfP + 4 <= 512, "TMEM budget");
 };
 
 __device__ __forceinline__ uint32_t swz_mode(int row_bytes) {
@@ -92,43 +108,42 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// work item w -> (bh, qt): longest causal query tiles first, heads innermost
+__device__ __forceinline__ void item_coords(const AttnParams& p, int w, int& bh, int& qt) {
+  const int r = w / p.n_bh;
+  bh = w - r * p.n_bh;
+  qt = p.causal ? p.n_qt - 1 - r : r;
+}
+
 template <int D, int DV, int LOW, bool PVBF16>
-__global__ void __launch_bounds__(256, 1) dma_attn_kernel(const __grid_constant__ AttnParams p) {
+__global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant__ AttnParams p) {
   using C = AttnCfg<D, DV, LOW, PVBF16>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::oBar);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;            // [kNK]
-  uint64_t* k_empty = bars + 1 + C::kNK;  // [kNK]
-  uint64_t* v_full = bars + 1 + 2 * C::kNK;
-  uint64_t* v_empty = v_full + C::kNV;
-  uint64_t* s_full = v_empty + C::kNV;  // [2]
+  uint64_t* q_full = bars + 0;                // [kNQ]
+  uint64_t* q_empty = q_full + C::kNQ;        // [kNQ]
+  uint64_t* k_full = q_empty + C::kNQ;        // [kNK]
+  uint64_t* k_empty = k_full + C::kNK;        // [kNK]
+  uint64_t* v_full = k_empty + C::kNK;        // [kNV]
+  uint64_t* v_empty = v_full + C::kNV;        // [kNV]
+  uint64_t* s_full = v_empty + C::kNV;        // [2]
   uint64_t* p_full = s_full + 2;
   uint64_t* o_done = p_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // ---- work item: heaviest causal query tile of each head first (LPT within a head)
-  const int item = blockIdx.x;
-  const int bh = item / p.n_qt;
-  const int qt = p.n_qt - 1 - (item % p.n_qt);
-  const int b = bh / p.heads, h = bh % p.heads;
-  const int mat_q = bh;
-  const int mat_k = b * p.kv_heads + h / p.group;
-  const int q0 = qt * C::kBM;
-  Plan plan;
-  plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
-  const int n_ent = plan.n;
   const int rt_q = p.lq_pad >> 7, rt_k = p.lk_pad >> 7;
 
   if (warp == 0) {
     if (lane == 0) {
-      ptx::mbar_init(q_full, 1);
+      for (int i = 0; i < C::kNQ; ++i) {
+        ptx::mbar_init(q_full + i, 1);
+        ptx::mbar_init(q_empty + i, 1);
+      }
       for (int i = 0; i < C::kNK; ++i) {
         ptx::mbar_init(k_full + i, 1);
-        ptx::mbar_init(k_empty + i, 1);
+        ptx::mbar_init(k_empty + i, 1 + 8);  // MMA commit + the 8 softmax warps (S_q^K reads)
       }
       for (int i = 0; i < C::kNV; ++i) {
         ptx::mbar_init(v_full + i, 1);
@@ -136,7 +151,7 @@ __global__ void __launch_bounds__(256, 1) dma_attn_kernel(const __grid_constant_
       }
       ptx::mbar_init(s_full + 0, 1);
       ptx::mbar_init(s_full + 1, 1);
-      ptx::mbar_init(p_full, 4);
+      ptx::mbar_init(p_full, 8);  // one arrive per softmax warp
       ptx::mbar_init(o_done, 1);
       ptx::fence_barrier_init();
       ptx::tma_prefetch_desc(&p.tm_q_hi);
@@ -151,10 +166,8 @@ __global__ void __launch_bounds__(256, 1) dma_attn_kernel(const __grid_constant_
     ptx::tmem_alloc<512>(tmem_slot);
   } else if (warp == 2 && !PVBF16) {
     // constant P scale-factor atom: E8M0 127 (= 1.0) for every row / k-block
-    reinterpret_cast<uint32_t*>(smem + C::oSfP)[lane] = 0x7F7F7F7Fu;
-    reinterpret_cast<uint32_t*>(smem + C::oSfP)[lane + 32] = 0x7F7F7F7Fu;
-    reinterpret_cast<uint32_t*>(smem + C::oSfP)[lane + 64] = 0x7F7F7F7Fu;
-    reinterpret_cast<uint32_t*>(smem + C::oSfP)[lane + 96] = 0x7F7F7F7Fu;
+    uint32_t* sfp = reinterpret_cast<uint32_t*>(smem + C::oSfP);
+    for (int i = lane; i < 128; i += 32) sfp[i] = 0x7F7F7F7Fu;
     ptx::fence_proxy_async_smem();
   }
   ptx::tc_fence_before();
@@ -164,84 +177,127 @@ __global__ void __launch_bounds__(256, 1) dma_attn_kernel(const __grid_constant_
 
   if (warp == 0) {
     // =========================== TMA producer ===========================
-    if (lane == 0 && n_ent > 0) {
-      uint32_t qbytes = C::kQHiBytes + 512 * C::kChHi;
-      if (LOW != kLowHigh) qbytes += C::kQLoBytes + 512 * C::kChLo;
-      ptx::mbar_arrive_expect_tx(q_full, qbytes);
-      ptx::tma_load_3d(smem + C::oQHi, &p.tm_q_hi, q_full, 0, q0, mat_q);
-      ptx::bulk_load(smem + C::oSfQHi, p.sf_q_hi + (static_cast<int64_t>(mat_q) * rt_q + qt) * p.ch_hi * 512,
-                     512 * C::kChHi, q_full);
-      if (LOW != kLowHigh) {
-        ptx::tma_load_3d(smem + C::oQLo, &p.tm_q_lo, q_full, 0, q0, mat_q);
-        ptx::bulk_load(smem + C::oSfQLo, p.sf_q_lo + (static_cast<int64_t>(mat_q) * rt_q + qt) * p.ch_lo * 512,
-                       512 * C::kChLo, q_full);
-      }
-      for (int e = 0; e < n_ent; ++e) {
-        int t;
-        bool hi;
-        plan.entry(e, t, hi);
-        if (LOW == kLowHigh) hi = true;
-        const int ks = e % C::kNK;
-        ptx::mbar_wait(k_empty + ks, ((e / C::kNK) & 1) ^ 1);
-        const int ch = hi ? C::kChHi : C::kChLo;
-        const uint32_t kb = hi ? C::kKBytes : C::kKBytes / 2;
-        ptx::mbar_arrive_expect_tx(k_full + ks, kb + 512 * ch + 512);
-        ptx::tma_load_3d(smem + C::oK + ks * C::kKStage, hi ? &p.tm_k_hi : &p.tm_k_lo, k_full + ks, 0,
-                         t * C::kBN, mat_k);
-        const uint8_t* sfsrc = (hi ? p.sf_k_hi : p.sf_k_lo) +
-                               (static_cast<int64_t>(mat_k) * rt_k + t) * (hi ? p.ch_hi : p.ch_lo) * 512;
-        ptx::bulk_load(smem + C::oSfK + ks * 512 * C::kChK, sfsrc, 512 * ch, k_full + ks);
-        ptx::bulk_load(smem + C::oSqK + ks * 512, p.qs_k + static_cast<int64_t>(mat_k) * p.lk_pad + t * C::kBN,
-                       512, k_full + ks);
+    if (lane == 0) {
+      uint32_t kc = 0, vc = 0, ic = 0;  // ring counters (continue across items)
+      for (int w = blockIdx.x; w < p.n_items; w += gridDim.x) {
+        int bh, qt;
+        item_coords(p, w, bh, qt);
+        const int b = bh / p.heads, h = bh % p.heads;
+        const int mat_q = bh, mat_k = b * p.kv_heads + h / p.group;
+        Plan plan;
+        plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
+        if (plan.n == 0) continue;  // nothing to load (the softmax side writes zeros)
+        const int qs = ic % C::kNQ;
+        ++ic;
+        ptx::mbar_wait(q_empty + qs, (((ic - 1) / C::kNQ) & 1) ^ 1);
+        uint32_t qbytes = C::kQHiBytes + 512 * C::kChHi;
+        if (LOW != kLowHigh) qbytes += C::kQLoBytes + 512 * C::kChLo;
+        uint8_t* qdst = smem + C::oQ + qs * C::kQStage;
+        uint8_t* sfq = smem + C::oSfQ + qs * C::kSfQStage;
+        ptx::mbar_arrive_expect_tx(q_full + qs, qbytes);
+        ptx::tma_load_3d(qdst, &p.tm_q_hi, q_full + qs, 0, qt * C::kBM, mat_q);
+        ptx::bulk_load(sfq, p.sf_q_hi + (static_cast<int64_t>(mat_q) * rt_q + qt) * p.ch_hi * 512,
+                       512 * C::kChHi, q_full + qs);
+        if (LOW != kLowHigh) {
+          ptx::tma_load_3d(qdst + C::kQHiBytes, &p.tm_q_lo, q_full + qs, 0, qt * C::kBM, mat_q);
+          ptx::bulk_load(sfq + 512 * C::kChHi, p.sf_q_lo + (static_cast<int64_t>(mat_q) * rt_q + qt) * p.ch_lo * 512,
+                         512 * C::kChLo, q_full + qs);
+        }
+        for (int e = 0; e < plan.n; ++e, ++kc, ++vc) {
+          int t;
+          bool hi;
+          plan.entry(e, t, hi);
+          if (LOW == kLowHigh) hi = true;
+          const int ks = kc % C::kNK;
+          ptx::mbar_wait(k_empty + ks, ((kc / C::kNK) & 1) ^ 1);
+          const int ch = hi ? C::kChHi : C::kChLo;
+          const uint32_t kb = hi ? C::kKBytes : C::kKBytes / 2;
+          ptx::mbar_arrive_expect_tx(k_full + ks, kb + 512 * ch + 512);
+          ptx::tma_load_3d(smem + C::oK + ks * C::kKBytes, hi ? &p.tm_k_hi : &p.tm_k_lo, k_full + ks, 0,
+                           t * C::kBN, mat_k);
+          const uint8_t* sfsrc = (hi ? p.sf_k_hi : p.sf_k_lo) +
+                                 (static_cast<int64_t>(mat_k) * rt_k + t) * (hi ? p.ch_hi : p.ch_lo) * 512;
+          ptx::bulk_load(smem + C::oSfK + ks * 512 * C::kChK, sfsrc, 512 * ch, k_full + ks);
+          ptx::bulk_load(smem + C::oSqK + ks * 512, p.qs_k + static_cast<int64_t>(mat_k) * p.lk_pad + t * C::kBN,
+                         512, k_full + ks);
 
-        const int vs = e % C::kNV;
-        ptx::mbar_wait(v_empty + vs, ((e / C::kNV) & 1) ^ 1);
-        uint8_t* vdst = smem + C::oV + vs * C::kVBytes;
-        if (PVBF16) {
-          ptx::mbar_arrive_expect_tx(v_full + vs, C::kVBytes);
+          const int vs = vc % C::kNV;
+          ptx::mbar_wait(v_empty + vs, ((vc / C::kNV) & 1) ^ 1);
+          uint8_t* vdst = smem + C::oV + vs * C::kVBytes;
+          if (PVBF16) {
+            ptx::mbar_arrive_expect_tx(v_full + vs, C::kVBytes);
 #pragma unroll
-          for (int half = 0; half < DV / 64; ++half)
-            ptx::tma_load_3d(vdst + half * (C::kBN * 128), &p.tm_v, v_full + vs, half * 64, t * C::kBN, mat_k);
-        } else {
-          ptx::mbar_arrive_expect_tx(v_full + vs, C::kVBytes + 512);
-          ptx::tma_load_3d(vdst, &p.tm_v, v_full + vs, 0, t * C::kBN, mat_k);
-          ptx::bulk_load(smem + C::oSfV + vs * 512, p.sf_v + (static_cast<int64_t>(mat_k) * rt_k + t) * 512, 512,
-                         v_full + vs);
+            for (int half = 0; half < DV / 64; ++half)
+              ptx::tma_load_3d(vdst + half * (C::kBN * 128), &p.tm_v, v_full + vs, half * 64, t * C::kBN, mat_k);
+          } else {
+            ptx::mbar_arrive_expect_tx(v_full + vs, C::kVBytes + 512);
+            ptx::tma_load_3d(vdst, &p.tm_v, v_full + vs, 0, t * C::kBN, mat_k);
+            ptx::bulk_load(smem + C::oSfV + vs * 512, p.sf_v + (static_cast<int64_t>(mat_k) * rt_k + t) * 512, 512,
+                           v_full + vs);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // =========================== MMA issuer ===========================
-    if (lane == 0 && n_ent > 0) {
-      ptx::mbar_wait(q_full, 0);
-      ptx::tc_fence_after();
-      for (int j = 0; j < C::kChHi; ++j)
-        ptx::tc_cp_sf(tmem + C::tSfQHi + 4 * j,
-                      ptx::smem_desc(ptx::smem_u32(smem + C::oSfQHi + 512 * j), 0, 128, ptx::kSwNone));
-      if (LOW != kLowHigh)
-        for (int j = 0; j < C::kChLo; ++j)
-          ptx::tc_cp_sf(tmem + C::tSfQLo + 4 * j,
-                        ptx::smem_desc(ptx::smem_u32(smem + C::oSfQLo + 512 * j), 0, 128, ptx::kSwNone));
+    if (lane == 0) {
       if (!PVBF16)
         ptx::tc_cp_sf(tmem + C::tSfP, ptx::smem_desc(ptx::smem_u32(smem + C::oSfP), 0, 128, ptx::kSwNone));
+      // The tile stream of this CTA, flattened across items.  QK of tile
+      // (g + 1) is issued before the PV of tile g (S is double buffered).
+      struct Cursor {
+        int w = 0, e = 0, n = 0;
+        uint32_t ic = 0;  // item ordinal in this CTA
+        Plan plan;
+      };
+      auto load_item = [&](Cursor& c) {  // advance c to the first item with a non-empty plan
+        while (c.w < p.n_items) {
+          int bh, qt;
+          item_coords(p, c.w, bh, qt);
+          c.plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
+          c.n = c.plan.n;
+          c.e = 0;
+          if (c.n > 0) return true;
+          c.w += gridDim.x;  // empty plan: nothing to issue (the softmax side writes zeros)
+        }
+        return false;
+      };
+      uint32_t kc = 0, vc = 0, g = 0;  // ring counters, tile ordinal
+      Cursor cq;  // next QK to issue
+      cq.w = blockIdx.x;
+      bool more = load_item(cq);
 
-      auto issue_qk = [&](int e) {
+      auto issue_qk = [&](Cursor& c, uint32_t tile_ord) {
+        const int qs = c.ic % C::kNQ;
+        if (c.e == 0) {
+          ptx::mbar_wait(q_full + qs, (c.ic / C::kNQ) & 1);
+          ptx::tc_fence_after();
+          const uint8_t* sfq = smem + C::oSfQ + qs * C::kSfQStage;
+          for (int j = 0; j < C::kChHi; ++j)
+            ptx::tc_cp_sf(tmem + C::tSfQ + 12 * qs + 4 * j,
+                          ptx::smem_desc(ptx::smem_u32(sfq + 512 * j), 0, 128, ptx::kSwNone));
+          if (LOW != kLowHigh)
+            for (int j = 0; j < C::kChLo; ++j)
+              ptx::tc_cp_sf(tmem + C::tSfQ + 12 * qs + 4 + 4 * j,
+                            ptx::smem_desc(ptx::smem_u32(sfq + 512 * (C::kChHi + j)), 0, 128, ptx::kSwNone));
+        }
         int t;
         bool hi;
-        plan.entry(e, t, hi);
+        c.plan.entry(c.e, t, hi);
         if (LOW == kLowHigh) hi = true;
-        const int ks = e % C::kNK;
-        ptx::mbar_wait(k_full + ks, (e / C::kNK) & 1);
+        const int ks = kc % C::kNK;
+        ptx::mbar_wait(k_full + ks, (kc / C::kNK) & 1);
         ptx::tc_fence_after();
-        const uint32_t tsfk = tmem + ((e & 1) ? C::tSfK1 : C::tSfK0);
+        const uint32_t tsfk = tmem + C::tSfK + 8 * (tile_ord & 1);
         const int ch = hi ? C::kChHi : C::kChLo;
         for (int j = 0; j < ch; ++j)
           ptx::tc_cp_sf(tsfk + 4 * j, ptx::smem_desc(ptx::smem_u32(smem + C::oSfK + ks * 512 * C::kChK + 512 * j),
                                                      0, 128, ptx::kSwNone));
-        const uint32_t tS = tmem + ((e & 1) ? C::tS1 : C::tS0);
-        const uint32_t kaddr = ptx::smem_u32(smem + C::oK + ks * C::kKStage);
+        const uint32_t tS = tmem + ((tile_ord & 1) ? C::tS1 : C::tS0);
+        const uint32_t kaddr = ptx::smem_u32(smem + C::oK + ks * C::kKBytes);
+        const uint32_t qaddr = ptx::smem_u32(smem + C::oQ + qs * C::kQStage);
+        const uint32_t tsfq = tmem + C::tSfQ + 12 * qs;
         if (hi) {
-          const uint32_t qaddr = ptx::smem_u32(smem + C::oQHi);
           constexpr int rb = D;  // fp8 row bytes
           const uint32_t sw = swz_mode(rb);
 #pragma unroll
@@ -250,231 +306,277 @@ __global__ void __launch_bounds__(256, 1) dma_attn_kernel(const __grid_constant_
             const uint64_t bd = ptx::smem_desc(kaddr + 32 * kk, 16, 8 * rb, sw);
             const uint32_t f = static_cast<uint32_t>(p.hfmt);
             const uint32_t id = ptx::idesc_bs(f, f, 0, 0, 128, 128, 1, kk & 3, kk & 3);
-            ptx::mma_mxf8f6f4(tS, ad, bd, id, tmem + C::tSfQHi + 4 * (kk >> 2), tsfk + 4 * (kk >> 2), kk > 0);
+            ptx::mma_mxf8f6f4(tS, ad, bd, id, tsfq + 4 * (kk >> 2), tsfk + 4 * (kk >> 2), kk > 0);
           }
         } else {
-          const uint32_t qaddr = ptx::smem_u32(smem + C::oQLo);
+          const uint32_t qlo = qaddr + C::kQHiBytes;
           constexpr int rb = D / 2;  // packed fp4 row bytes
           const uint32_t sw = swz_mode(rb);
 #pragma unroll
           for (int kk = 0; kk < D / 64; ++kk) {
-            const uint64_t ad = ptx::smem_desc(qaddr + 32 * kk, 16, 8 * rb, sw);
+            const uint64_t ad = ptx::smem_desc(qlo + 32 * kk, 16, 8 * rb, sw);
             const uint64_t bd = ptx::smem_desc(kaddr + 32 * kk, 16, 8 * rb, sw);
             if (LOW == kLowNV) {
               const uint32_t id = ptx::idesc_bs(1, 1, 0, 0, 128, 128, 0, 0, 0);
-              ptx::mma_nvf4(tS, ad, bd, id, tmem + C::tSfQLo + 4 * kk, tsfk + 4 * kk, kk > 0);
+              ptx::mma_nvf4(tS, ad, bd, id, tsfq + 4 + 4 * kk, tsfk + 4 * kk, kk > 0);
             } else {
               const uint32_t sid = (kk & 1) * 2;
               const uint32_t id = ptx::idesc_bs(1, 1, 0, 0, 128, 128, 1, sid, sid);
-              ptx::mma_mxf4(tS, ad, bd, id, tmem + C::tSfQLo + 4 * (kk >> 1), tsfk + 4 * (kk >> 1), kk > 0);
+              ptx::mma_mxf4(tS, ad, bd, id, tsfq + 4 + 4 * (kk >> 1), tsfk + 4 * (kk >> 1), kk > 0);
             }
           }
         }
         ptx::tc_commit(k_empty + ks);
-        ptx::tc_commit(s_full + (e & 1));
+        ptx::tc_commit(s_full + (tile_ord & 1));
+        ++kc;
+        if (++c.e == c.n) {
+          ptx::tc_commit(q_empty + qs);  // Q smem free once these MMAs complete
+          c.w += gridDim.x;
+          ++c.ic;
+          return load_item(c);
+        }
+        return true;
       };
 
-      issue_qk(0);
-      for (int e = 0; e < n_ent; ++e) {
-        if (e + 1 < n_ent) issue_qk(e + 1);
-        ptx::mbar_wait(p_full, e & 1);
+      // PV cursor trails the QK cursor by one tile
+      Cursor cp = cq;
+      if (more) more = issue_qk(cq, 0);
+      bool pv_more = cp.w < p.n_items && cp.n > 0;
+      while (pv_more) {
+        if (more) more = issue_qk(cq, g + 1);
+        ptx::mbar_wait(p_full, g & 1);
         ptx::tc_fence_after();
-        const int vs = e % C::kNV;
-        ptx::mbar_wait(v_full + vs, (e / C::kNV) & 1);
+        const int vs = vc % C::kNV;
+        ptx::mbar_wait(v_full + vs, (vc / C::kNV) & 1);
         ptx::tc_fence_after();
-        const uint32_t tP = tmem + ((e & 1) ? C::tS1 : C::tS0);
+        const uint32_t tP = tmem + ((g & 1) ? C::tS1 : C::tS0);
         const uint32_t vaddr = ptx::smem_u32(smem + C::oV + vs * C::kVBytes);
+        const bool first = cp.e == 0;
         if (PVBF16) {
 #pragma unroll
           for (int kk = 0; kk < C::kBN / 16; ++kk) {
             const uint64_t bd = ptx::smem_desc(vaddr + kk * 16 * 128, C::kBN * 128, 1024, ptx::kSw128);
-            ptx::mma_f16_ts(tmem + C::tO, tP + 8 * kk, bd, ptx::idesc_bf16(0, 1, 128, DV), (e > 0 || kk > 0));
+            const uint32_t pa = tP + 64 * (kk >> 2) + 8 * (kk & 3);
+            ptx::mma_f16_ts(tmem + C::tO, pa, bd, ptx::idesc_bf16(0, 1, 128, DV), !(first && kk == 0));
           }
         } else {
-          const uint32_t tsfv = tmem + ((e & 1) ? C::tSfV1 : C::tSfV0);
+          const uint32_t tsfv = tmem + C::tSfV + 4 * (g & 1);
           ptx::tc_cp_sf(tsfv, ptx::smem_desc(ptx::smem_u32(smem + C::oSfV + vs * 512), 0, 128, ptx::kSwNone));
           constexpr int rb = DV;  // fp8 V row bytes (MN-major)
 #pragma unroll
           for (int kk = 0; kk < C::kBN / 32; ++kk) {
             const uint64_t bd = ptx::smem_desc(vaddr + kk * 32 * rb, 16, 8 * rb, swz_mode(rb));
             const uint32_t id = ptx::idesc_bs(0, 0, 0, 1, 128, DV, 1, kk & 3, kk & 3);
-            ptx::mma_mxf8f6f4_ts(tmem + C::tO, tP + 8 * kk, bd, id, tmem + C::tSfP, tsfv, (e > 0 || kk > 0));
+            const uint32_t pa = tP + 64 * (kk >> 1) + 8 * (kk & 1);
+            ptx::mma_mxf8f6f4_ts(tmem + C::tO, pa, bd, id, tmem + C::tSfP, tsfv, !(first && kk == 0));
           }
         }
         ptx::tc_commit(v_empty + vs);
         ptx::tc_commit(o_done);
+        ++vc;
+        ++g;
+        if (++cp.e == cp.n) {
+          cp.w += gridDim.x;
+          ++cp.ic;
+          pv_more = load_item(cp);
+        }
       }
     }
     __syncwarp();
   } else if (warp >= 4) {
     // =========================== softmax / correction / epilogue ===========================
-    const int r = threadIdx.x - 128;  // query row within the tile == TMEM lane
-    const uint32_t lane_base = static_cast<uint32_t>((warp - 4) * 32) << 16;
-    const int qrow = q0 + r;
-    const float sq_q = (qrow < p.lq) ? p.qs_q[static_cast<int64_t>(mat_q) * p.lq_pad + qrow] : 1.0f;
-    float m_run = -INFINITY, l_run = 0.f;
+    const int half = (warp - 4) >> 2;          // key columns [64 half, 64 half + 64)
+    const int quad = warp & 3;                  // TMEM lane quadrant
+    const int r = quad * 32 + lane;             // query row within the tile == TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t bar_id = 1 + quad;           // partner warps (4 + quad, 8 + quad)
+    float* red = reinterpret_cast<float*>(smem + C::oRed);
+    float* red_l = reinterpret_cast<float*>(smem + C::oRedL);
     constexpr float kPShift = PVBF16 ? 0.f : 8.f;  // P stored as E4M3(P * 2^8)
+    constexpr int kOC = DV / 2;                     // O columns owned by this half
+    uint32_t g = 0;                                 // tile ordinal (matches the MMA issuer)
 
-    for (int e = 0; e < n_ent; ++e) {
-      int t;
-      bool hi;
-      plan.entry(e, t, hi);
-      if (LOW == kLowHigh) hi = true;
-      const bool two_level = hi || (LOW == kLowNV);
-      const int k0 = t * C::kBN;
-      ptx::mbar_wait(s_full + (e & 1), (e >> 1) & 1);
-      ptx::tc_fence_after();
-      const uint32_t tS = tmem + ((e & 1) ? C::tS1 : C::tS0) + lane_base;
-      float s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t rr[32];
-        ptx::tmem_ld32(tS + 32 * c, rr);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[32 * c + i] = __uint_as_float(rr[i]);
-      }
-      ptx::tmem_ld_wait();
+    for (int w = blockIdx.x; w < p.n_items; w += gridDim.x) {
+      int bh, qt;
+      item_coords(p, w, bh, qt);
+      const int q0 = qt * C::kBM;
+      const int qrow = q0 + r;
+      Plan plan;
+      plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
+      const float sq_q = (qrow < p.lq) ? p.qs_q[static_cast<int64_t>(bh) * p.lq_pad + qrow] : 1.0f;
+      float m_run = -INFINITY;
+      float2 l2 = make_float2(0.f, 0.f);
 
-      // S_q^K column factors for two-level tiles (staged by the producer with the K tile)
-      const float rowf = two_level ? sq_q : 1.0f;
-      if (two_level) {
-        const float4* sqk = reinterpret_cast<const float4*>(smem + C::oSqK + (e % C::kNK) * 512);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float4 f = sqk[j];
-          s[4 * j + 0] *= f.x;
-          s[4 * j + 1] *= f.y;
-          s[4 * j + 2] *= f.z;
-          s[4 * j + 3] *= f.w;
-        }
-      }
-      // causal (attention.py:178-184, applied when k1-1 > q0, :306) and ragged-key masks
-      const int kvalid = p.lk - k0;  // keys [k0, k0+kvalid) exist
-      const bool need_causal = p.causal && (k0 + (kvalid < C::kBN ? kvalid : C::kBN) - 1 > q0);
-      if (need_causal || kvalid < C::kBN) {
-        const int lim = need_causal ? min(qrow - k0 + 1, kvalid) : kvalid;  // keep j < lim
-#pragma unroll
-        for (int j = 0; j < 128; ++j)
-          if (j >= lim) s[j] = -INFINITY;
-      }
-      float mx = -INFINITY;
-#pragma unroll
-      for (int j = 0; j < 128; ++j) mx = fmaxf(mx, s[j]);
-      const float m_tile = mx * rowf;
-      const float m_new = fmaxf(m_run, m_tile);
-      const bool dead = (m_new == -INFINITY);
-      const float alpha = dead ? 1.0f : fast_exp2(m_run - m_new);  // m_run = -inf -> 0
-      const float bias = dead ? 0.f : (kPShift - m_new);
-      float lsum = 0.f;
-      if (PVBF16) {
-        uint32_t pk[64];
-#pragma unroll
-        for (int j = 0; j < 64; ++j) {
-          const float p0 = fast_exp2(fmaf(s[2 * j], rowf, bias));
-          const float p1 = fast_exp2(fmaf(s[2 * j + 1], rowf, bias));
-          lsum += p0 + p1;
-          __nv_bfloat162 v = __floats2bfloat162_rn(p0, p1);
-          pk[j] = *reinterpret_cast<uint32_t*>(&v);
-        }
-        const uint32_t tP = tmem + ((e & 1) ? C::tS1 : C::tS0) + lane_base;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t w[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) w[i] = pk[16 * c + i];
-          ptx::tmem_st16(tP + 16 * c, w);
-        }
-      } else {
-        uint32_t pk[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float p0 = fast_exp2(fmaf(s[4 * j + 0], rowf, bias));
-          const float p1 = fast_exp2(fmaf(s[4 * j + 1], rowf, bias));
-          const float p2 = fast_exp2(fmaf(s[4 * j + 2], rowf, bias));
-          const float p3 = fast_exp2(fmaf(s[4 * j + 3], rowf, bias));
-          lsum += (p0 + p1) + (p2 + p3);
-          pk[j] = static_cast<uint32_t>(ptx::cvt_e4m3x2(p0, p1)) | (static_cast<uint32_t>(ptx::cvt_e4m3x2(p2, p3)) << 16);
-        }
-        const uint32_t tP = tmem + ((e & 1) ? C::tS1 : C::tS0) + lane_base;
-        uint32_t w0[16], w1[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          w0[i] = pk[i];
-          w1[i] = pk[16 + i];
-        }
-        ptx::tmem_st16(tP, w0);
-        ptx::tmem_st16(tP + 16, w1);
-      }
-      l_run = l_run * alpha + lsum;
-      m_run = m_new;
-      // O *= alpha once the previous PV has landed (rows whose max moved)
-      if (e > 0) {
-        ptx::mbar_wait(o_done, (e - 1) & 1);
+      for (int e = 0; e < plan.n; ++e, ++g) {
+        int t;
+        bool hi;
+        plan.entry(e, t, hi);
+        if (LOW == kLowHigh) hi = true;
+        const bool two_level = hi || (LOW == kLowNV);
+        const int k0 = t * C::kBN;
+        ptx::mbar_wait(s_full + (g & 1), (g >> 1) & 1);
         ptx::tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.0f)) {
-          const uint32_t tO = tmem + C::tO + lane_base;
+        const uint32_t tS = tmem + ((g & 1) ? C::tS1 : C::tS0) + lane_base + 64 * half;
+        float s[64];
+        {
+          uint32_t r0[32], r1[32];
+          ptx::tmem_ld32(tS, r0);
+          ptx::tmem_ld32(tS + 32, r1);
+          ptx::tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < DV / 32; ++c) {
-            uint32_t rr[32];
-            ptx::tmem_ld32(tO + 32 * c, rr);
-            ptx::tmem_ld_wait();
-            uint32_t w0[16], w1[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              w0[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
-              w1[i] = __float_as_uint(__uint_as_float(rr[16 + i]) * alpha);
-            }
-            ptx::tmem_st16(tO + 32 * c, w0);
-            ptx::tmem_st16(tO + 32 * c + 16, w1);
+          for (int i = 0; i < 32; ++i) {
+            s[i] = __uint_as_float(r0[i]);
+            s[32 + i] = __uint_as_float(r1[i]);
           }
         }
-      }
-      ptx::tmem_st_wait();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(p_full);
-    }
-
-    // ---- epilogue: O / l (attention.py:104-106)
-    float inv_l = 1.0f / (l_run > 0.f ? l_run : 1.0f);
-    if (n_ent > 0) {
-      ptx::mbar_wait(o_done, (n_ent - 1) & 1);
-      ptx::tc_fence_after();
-    }
-    const uint32_t tO = tmem + C::tO + lane_base;
-    const int64_t orow = static_cast<int64_t>(mat_q) * p.lq + qrow;
+        // S_q^K column factors for two-level tiles (staged by the producer with the K tile)
+        const float rowf = two_level ? sq_q : 1.0f;
+        if (two_level) {
+          const float4* sqk = reinterpret_cast<const float4*>(smem + C::oSqK + ((g % C::kNK) * 512)) + 16 * half;
 #pragma unroll
-    for (int c = 0; c < DV / 32; ++c) {
-      uint32_t rr[32];
-      if (n_ent > 0) {
-        ptx::tmem_ld32(tO + 32 * c, rr);
-        ptx::tmem_ld_wait();
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) rr[i] = 0u;
-      }
-      if (qrow < p.lq) {
-        if (p.out_bf16) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o) + orow * DV + 32 * c);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            uint32_t w[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(rr[8 * i + 2 * k]) * inv_l,
-                                                       __uint_as_float(rr[8 * i + 2 * k + 1]) * inv_l);
-              w[k] = *reinterpret_cast<uint32_t*>(&v);
-            }
-            dst[i] = make_uint4(w[0], w[1], w[2], w[3]);
+          for (int j = 0; j < 16; ++j) {
+            const float4 f = sqk[j];
+            float2 a = __fmul2_rn(make_float2(s[4 * j], s[4 * j + 1]), make_float2(f.x, f.y));
+            float2 b = __fmul2_rn(make_float2(s[4 * j + 2], s[4 * j + 3]), make_float2(f.z, f.w));
+            s[4 * j] = a.x; s[4 * j + 1] = a.y; s[4 * j + 2] = b.x; s[4 * j + 3] = b.y;
           }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(k_empty + (g % C::kNK));  // done with this K slot's S_q^K
+        // causal (attention.py:178-184, applied when k1-1 > q0, :306) and ragged-key masks
+        const int kvalid = p.lk - k0;  // keys [k0, k0+kvalid) exist
+        const bool need_causal = p.causal && (k0 + (kvalid < C::kBN ? kvalid : C::kBN) - 1 > q0);
+        const bool masked = need_causal || kvalid < C::kBN;
+        if (masked) {
+          const int lim = (need_causal ? min(qrow - k0 + 1, kvalid) : kvalid) - 64 * half;  // keep j < lim
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j >= lim) s[j] = -INFINITY;
+        }
+        float mx = fmaxf(s[0], s[1]);
+#pragma unroll
+        for (int j = 2; j < 64; j += 2) mx = ptx::fmax3(mx, s[j], s[j + 1]);
+        // row max across the two halves
+        float* rb = red + (g & 1) * 256;
+        rb[half * 128 + r] = mx;
+        ptx::named_bar_sync(bar_id, 64);
+        mx = fmaxf(mx, rb[(half ^ 1) * 128 + r]);
+        const float m_tile = mx * rowf;
+        const float m_new = fmaxf(m_run, m_tile);
+        const bool dead = (m_new == -INFINITY);
+        const float alpha = dead ? 1.0f : fast_exp2(m_run - m_new);  // m_run = -inf -> 0
+        const float bias = dead ? 0.f : (kPShift - m_new);
+        const float2 rf2 = make_float2(rowf, rowf), b2 = make_float2(bias, bias);
+        float2 ls = make_float2(0.f, 0.f);
+        const uint32_t tP = tmem + ((g & 1) ? C::tS1 : C::tS0) + lane_base + 64 * half;
+        if (PVBF16) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float2 x = __ffma2_rn(make_float2(s[2 * j], s[2 * j + 1]), rf2, b2);
+            x.x = fast_exp2(x.x);
+            x.y = fast_exp2(x.y);
+            ls = __fadd2_rn(ls, x);
+            __nv_bfloat162 v = __floats2bfloat162_rn(x.x, x.y);
+            pk[j] = *reinterpret_cast<uint32_t*>(&v);
+          }
+          ptx::tmem_st32(tP, pk);
         } else {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.o) + orow * DV + 32 * c);
+          uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            dst[i] = make_float4(__uint_as_float(rr[4 * i]) * inv_l, __uint_as_float(rr[4 * i + 1]) * inv_l,
-                                 __uint_as_float(rr[4 * i + 2]) * inv_l, __uint_as_float(rr[4 * i + 3]) * inv_l);
+          for (int j = 0; j < 16; ++j) {
+            float2 x0 = __ffma2_rn(make_float2(s[4 * j], s[4 * j + 1]), rf2, b2);
+            float2 x1 = __ffma2_rn(make_float2(s[4 * j + 2], s[4 * j + 3]), rf2, b2);
+            x0.x = fast_exp2(x0.x);
+            x0.y = fast_exp2(x0.y);
+            x1.x = fast_exp2(x1.x);
+            x1.y = fast_exp2(x1.y);
+            ls = __fadd2_rn(ls, __fadd2_rn(x0, x1));
+            pk[j] = static_cast<uint32_t>(ptx::cvt_e4m3x2(x0.x, x0.y)) |
+                    (static_cast<uint32_t>(ptx::cvt_e4m3x2(x1.x, x1.y)) << 16);
+          }
+          ptx::tmem_st16(tP, pk);
+        }
+        l2 = __ffma2_rn(l2, make_float2(alpha, alpha), ls);
+        m_run = m_new;
+        // O *= alpha once the previous PV has landed (rows whose max moved)
+        if (e > 0) {
+          ptx::mbar_wait(o_done, (g - 1) & 1);
+          ptx::tc_fence_after();
+          if (__any_sync(0xffffffffu, alpha != 1.0f)) {
+            const uint32_t tO = tmem + C::tO + lane_base + kOC * half;
+            const float2 a2 = make_float2(alpha, alpha);
+#pragma unroll
+            for (int c = 0; c < kOC / 32; ++c) {
+              uint32_t rr[32];
+              ptx::tmem_ld32(tO + 32 * c, rr);
+              ptx::tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                float2 v = __fmul2_rn(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])), a2);
+                rr[2 * i] = __float_as_uint(v.x);
+                rr[2 * i + 1] = __float_as_uint(v.y);
+              }
+              ptx::tmem_st32(tO + 32 * c, rr);
+            }
+          }
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(p_full);
+      }
+
+      // ---- epilogue: O / l (attention.py:104-106); l = sum of both halves
+      float l_part = l2.x + l2.y;
+      red_l[half * 128 + r] = l_part;
+      ptx::named_bar_sync(bar_id, 64);
+      const float l_run = l_part + red_l[(half ^ 1) * 128 + r];
+      ptx::named_bar_sync(bar_id, 64);  // red_l reusable by the next item
+      const float inv_l = 1.0f / (l_run > 0.f ? l_run : 1.0f);
+      if (plan.n > 0) {
+        ptx::mbar_wait(o_done, (g - 1) & 1);
+        ptx::tc_fence_after();
+      }
+      const uint32_t tO = tmem + C::tO + lane_base + kOC * half;
+      const int64_t orow = static_cast<int64_t>(bh) * p.lq + qrow;
+#pragma unroll
+      for (int c = 0; c < kOC / 32; ++c) {
+        uint32_t rr[32];
+        if (plan.n > 0) {
+          ptx::tmem_ld32(tO + 32 * c, rr);
+          ptx::tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) rr[i] = 0u;
+        }
+        if (qrow < p.lq) {
+          const int col = kOC * half + 32 * c;
+          if (p.out_bf16) {
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o) + orow * DV + col);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              uint32_t wv[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(rr[8 * i + 2 * k]) * inv_l,
+                                                         __uint_as_float(rr[8 * i + 2 * k + 1]) * inv_l);
+                wv[k] = *reinterpret_cast<uint32_t*>(&v);
+              }
+              dst[i] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            }
+          } else {
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.o) + orow * DV + col);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              dst[i] = make_float4(__uint_as_float(rr[4 * i]) * inv_l, __uint_as_float(rr[4 * i + 1]) * inv_l,
+                                   __uint_as_float(rr[4 * i + 2]) * inv_l, __uint_as_float(rr[4 * i + 3]) * inv_l);
+          }
         }
       }
+      // the next item's first PV overwrites O: the p_full arrive of its first tile
+      // (issued after these tcgen05.ld completed) orders it after this read
+      ptx::tc_fence_before();
     }
   }
 

@@ -222,13 +222,26 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
   return 0;
 }
 
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 template <int D, int LOW, bool PVBF16>
 static int launch_attn(const AttnParams& p, int64_t items, cudaStream_t st) {
   using C = AttnCfg<D, D, LOW, PVBF16>;
   auto kern = dma_attn_kernel<D, D, LOW, PVBF16>;
   const int smem = C::kSmemBytes > 120 * 1024 ? C::kSmemBytes : 120 * 1024;  // one CTA per SM (TMEM 512 cols)
   DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<static_cast<unsigned>(items), 256, smem, st>>>(p);
+  // persistent: one CTA per SM, items strided across CTAs (longest first)
+  const int64_t grid = items < num_sms() ? items : num_sms();
+  kern<<<static_cast<unsigned>(grid), 384, smem, st>>>(p);
   DMA_LAUNCH_CHECK();
   ++g_launches;
   return 0;
@@ -284,6 +297,9 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
   p.hfmt = a->high_format == DMA_FMT_MXFP8_E5M2 ? 1 : 0;
   const int64_t items = L.mq * p.n_qt;
   if (items == 0) return 0;
+  DMA_CHECK_ARG(items < (int64_t(1) << 31), "too many work items");
+  p.n_bh = static_cast<int>(L.mq);
+  p.n_items = static_cast<int>(items);
   const int low = a->low_format == DMA_FMT_NVFP4 ? kLowNV : (a->low_format == DMA_FMT_MXFP4 ? kLowMX4 : kLowHigh);
   return D == 64 ? dispatch_attn<64>(p, low, L.pv_bf16, items, st) : dispatch_attn<128>(p, low, L.pv_bf16, items, st);
 }
