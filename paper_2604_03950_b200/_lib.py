@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdma.so")
+LIB_PATH = os.environ.get("DMA_LIB_PATH") or os.path.join(_HERE, "libdma.so")
 
 DMA_EINVAL = -1
 DMA_EUNSUPPORTED = -2

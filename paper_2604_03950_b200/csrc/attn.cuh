@@ -108,12 +108,37 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe for a pair (x <= 0; masked -inf inputs never reach it):
+// x = n + f with n = floor(x) (round-down add of 1.5*2^23), f in [0, 1);
+// 2^f by a degree-4 polynomial (max rel. error 3e-6, below the E4M3 / bf16
+// rounding of P), 2^n added to the exponent field.  Offloads MUFU.EX2
+// (16/clk/SM), the softmax's throughput limit.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rd(x, magic);
+  const float2 fl = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-fl.x, -fl.y));
+  float2 p = __ffma2_rn(make_float2(0.013426235f, 0.013426235f), f, make_float2(0.052243195f, 0.052243195f));
+  p = __ffma2_rn(p, f, make_float2(0.24127987f, 0.24127987f));
+  p = __ffma2_rn(p, f, make_float2(0.6930449f, 0.6930449f));
+  p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+
 // work item w -> (bh, qt): longest causal query tiles first, heads innermost
 __device__ __forceinline__ void item_coords(const AttnParams& p, int w, int& bh, int& qt) {
   const int r = w / p.n_bh;
   bh = w - r * p.n_bh;
   qt = p.causal ? p.n_qt - 1 - r : r;
 }
+
+#ifndef DMA_POLY_PAIRS
+#define DMA_POLY_PAIRS 3  // 2 * DMA_POLY_PAIRS of every 16 exponentials go to the FMA pipe
+#endif
+constexpr int kPolyPairs = DMA_POLY_PAIRS;
 
 template <int D, int DV, int LOW, bool PVBF16>
 __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant__ AttnParams p) {
@@ -487,8 +512,12 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
           for (int j = 0; j < 16; ++j) {
             float2 x0 = __ffma2_rn(make_float2(s[4 * j], s[4 * j + 1]), rf2, b2);
             float2 x1 = __ffma2_rn(make_float2(s[4 * j + 2], s[4 * j + 3]), rf2, b2);
-            x0.x = fast_exp2(x0.x);
-            x0.y = fast_exp2(x0.y);
+            if (!masked && (j % 4) < kPolyPairs) {  // FMA-pipe exp2 on a fixed share of the pairs
+              x0 = exp2_poly2(x0);
+            } else {
+              x0.x = fast_exp2(x0.x);
+              x0.y = fast_exp2(x0.y);
+            }
             x1.x = fast_exp2(x1.x);
             x1.y = fast_exp2(x1.y);
             ls = __fadd2_rn(ls, __fadd2_rn(x0, x1));

@@ -1,0 +1,591 @@
+// Phase 2 of the DMA forward, ping-pong variant (block-scaled MXFP8 PV).
+//
+// Same algorithm as attn.cuh (attention.py:282-310 with the plans of
+// attention.py:191-233 and the base-2 online softmax of :150-175), organised
+// for overlap: every CTA runs TWO independent query-tile streams A and B,
+// each with its own softmax warpgroup, so that one stream's exp2 phase
+// (MUFU-bound) overlaps the other's TMEM loads / max / bookkeeping.
+//
+// Work unit = a *pair*: the same 128-row query tile of two heads (bh, bh+1).
+// Both heads have the same tile plan, so the two streams walk identical
+// (key tile, precision) sequences; with GQA they usually share the KV head,
+// and then every K / V tile is loaded once and used by both.  Pairs are
+// handed out dynamically (global atomic ticket), head-major when the K/V
+// footprint exceeds L2 (the 148 CTAs then stream the same K/V), otherwise
+// longest-causal-tile first.
+//
+// TMEM (512 columns), one S buffer shared by the streams:
+//   S [0,128)  P_A [128,160)  P_B [160,192)  O_A [192,+DV)  O_B [320,+DV)
+//   SF: Q_A 448 | Q_B 460 | K_A 472 | K_B 480 | V_A 488 | V_B 492 | P 496
+// The MMA issuer runs QK_A(0) QK_B(0) { QK_A(j+1) PV_A(j) QK_B(j+1) PV_B(j) }:
+// a QK waits until the previous S consumer has copied S into registers.
+//
+// Warps: 0 producer (TMA + scheduler), 1 MMA issuer, 2-3 idle,
+//        4-7 softmax stream A, 8-11 softmax stream B (one query row per thread).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "attn.cuh"
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace dma {
+
+struct PPParams {
+  int n_pairs;
+  int pairs_per_qt;
+  int head_major;
+  unsigned int* ticket;  // [0] next pair, [1] CTAs done (self-resetting)
+};
+
+template <int D, int DV, int LOW>
+struct PPCfg {
+  static constexpr int kBM = 128, kBN = 128;
+  static constexpr int kNK = 4, kNV = 3, kNS = 4, kNSch = 4;
+  static constexpr int kQHiBytes = kBM * D;
+  static constexpr int kQLoBytes = kBM * D / 2;
+  static constexpr int kQStream = ((kQHiBytes + (LOW != kLowHigh ? kQLoBytes : 0) + 1023) / 1024) * 1024;
+  static constexpr int kKBytes = kBN * D;
+  static constexpr int kVBytes = kBN * DV;
+  static constexpr int kChHi = (D / 32 + 3) / 4;
+  static constexpr int kChLo = LOW == kLowNV ? (D / 16 + 3) / 4 : (D / 32 + 3) / 4;
+  static constexpr int kChK = kChHi > kChLo ? kChHi : kChLo;
+  static constexpr int kSfQ = 512 * (kChHi + kChLo);
+  // smem (offsets from a 1024-aligned base)
+  static constexpr int oQ = 0;                                // [2 slot][2 stream][kQStream]
+  static constexpr int oK = oQ + 4 * kQStream;                // [kNK][kKBytes]
+  static constexpr int oV = oK + kNK * kKBytes;               // [kNV][kVBytes]
+  static constexpr int oSfQ = oV + kNV * kVBytes;             // [2 slot][2 stream][kSfQ]
+  static constexpr int oSfK = oSfQ + 4 * kSfQ;                // [kNK][kChK][512]
+  static constexpr int oSfV = oSfK + kNK * kChK * 512;        // [kNV][512]
+  static constexpr int oSqK = oSfV + kNV * 512;               // [2 stream][kNS][512]
+  static constexpr int oSfP = oSqK + 2 * kNS * 512;           // 512
+  static constexpr int oSch = oSfP + 512;                     // [kNSch] int
+  static constexpr int oBar = oSch + 64;
+  static constexpr int kSmemBytes = oBar + 512 + 1024;
+  // TMEM columns
+  static constexpr uint32_t tS = 0, tSfP = 496;
+  __device__ static constexpr uint32_t tP(int x) { return 128u + 32u * x; }
+  __device__ static constexpr uint32_t tO(int x) { return 192u + 128u * x; }
+  __device__ static constexpr uint32_t tSfQ(int x) { return 448u + 12u * x; }
+  __device__ static constexpr uint32_t tSfK(int x) { return 472u + 8u * x; }
+  __device__ static constexpr uint32_t tSfV(int x) { return 488u + 4u * x; }
+};
+
+__device__ __forceinline__ void pair_coords(const AttnParams& p, const PPParams& q, int k, int& bh0, int& bh1,
+                                            int& qt) {
+  int r, hp;
+  if (q.head_major) {
+    hp = k / p.n_qt;
+    r = k - hp * p.n_qt;
+  } else {
+    r = k / q.pairs_per_qt;
+    hp = k - r * q.pairs_per_qt;
+  }
+  qt = p.causal ? p.n_qt - 1 - r : r;
+  bh0 = 2 * hp;
+  bh1 = 2 * hp + 1 < p.n_bh ? 2 * hp + 1 : -1;
+}
+
+__device__ __forceinline__ int mat_k_of(const AttnParams& p, int bh) {
+  const int b = bh / p.heads, h = bh - b * p.heads;
+  return b * p.kv_heads + h / p.group;
+}
+
+template <int D, int DV, int LOW>
+__global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_constant__ AttnParams p,
+                                                             const __grid_constant__ PPParams pp) {
+  using C = PPCfg<D, DV, LOW>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::oBar);
+  uint64_t* q_full = bars;                        // [2]
+  uint64_t* q_empty = q_full + 2;                 // [2]
+  uint64_t* k_full = q_empty + 2;                 // [kNK]
+  uint64_t* k_empty = k_full + C::kNK;            // [kNK]
+  uint64_t* v_full = k_empty + C::kNK;            // [kNV]
+  uint64_t* v_empty = v_full + C::kNV;            // [kNV]
+  uint64_t* sq_empty = v_empty + C::kNV;          // [2][kNS]
+  uint64_t* s_free = sq_empty + 2 * C::kNS;       // 1
+  uint64_t* s_full = s_free + 1;                  // [2]
+  uint64_t* p_full = s_full + 2;                  // [2]
+  uint64_t* o_done = p_full + 2;                  // [2]
+  uint64_t* sch_full = o_done + 2;                // [kNSch]
+  uint64_t* sch_empty = sch_full + C::kNSch;      // [kNSch]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sch_empty + C::kNSch);
+  int* sched = reinterpret_cast<int*>(smem + C::oSch);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rt_q = p.lq_pad >> 7, rt_k = p.lk_pad >> 7;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < 2; ++i) {
+        ptx::mbar_init(q_full + i, 1);
+        ptx::mbar_init(q_empty + i, 1);
+        ptx::mbar_init(s_full + i, 1);
+        ptx::mbar_init(p_full + i, 4);
+        ptx::mbar_init(o_done + i, 1);
+      }
+      for (int i = 0; i < C::kNK; ++i) {
+        ptx::mbar_init(k_full + i, 1);
+        ptx::mbar_init(k_empty + i, 1);
+      }
+      for (int i = 0; i < C::kNV; ++i) {
+        ptx::mbar_init(v_full + i, 1);
+        ptx::mbar_init(v_empty + i, 1);
+      }
+      for (int i = 0; i < 2 * C::kNS; ++i) ptx::mbar_init(sq_empty + i, 4);
+      ptx::mbar_init(s_free, 4);
+      for (int i = 0; i < C::kNSch; ++i) {
+        ptx::mbar_init(sch_full + i, 1);
+        ptx::mbar_init(sch_empty + i, 1 + 8);
+      }
+      ptx::fence_barrier_init();
+      ptx::tma_prefetch_desc(&p.tm_q_hi);
+      ptx::tma_prefetch_desc(&p.tm_k_hi);
+      ptx::tma_prefetch_desc(&p.tm_v);
+      if (LOW != kLowHigh) {
+        ptx::tma_prefetch_desc(&p.tm_q_lo);
+        ptx::tma_prefetch_desc(&p.tm_k_lo);
+      }
+    }
+  } else if (warp == 1) {
+    ptx::tmem_alloc<512>(tmem_slot);
+  } else if (warp == 2) {
+    // constant P scale-factor atom: E8M0 127 (= 1.0) for every row / k-block
+    uint32_t* sfp = reinterpret_cast<uint32_t*>(smem + C::oSfP);
+    for (int i = lane; i < 128; i += 32) sfp[i] = 0x7F7F7F7Fu;
+    ptx::fence_proxy_async_smem();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // =========================== scheduler + TMA producer ===========================
+    if (lane == 0) {
+      uint32_t kc = 0, vc = 0, sc[2] = {0, 0}, po = 0;
+      for (uint32_t i = 0;; ++i) {
+        const int ss = i % C::kNSch;
+        ptx::mbar_wait(sch_empty + ss, ((i / C::kNSch) & 1) ^ 1);
+        const unsigned int tk = atomicAdd(pp.ticket, 1u);
+        const int k = tk < static_cast<unsigned int>(pp.n_pairs) ? static_cast<int>(tk) : -1;
+        sched[ss] = k;
+        ptx::mbar_arrive(sch_full + ss);  // release: the slot write is visible to waiters
+        if (k < 0) break;
+        int bh[2], qt;
+        pair_coords(p, pp, k, bh[0], bh[1], qt);
+        Plan plan;
+        plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
+        if (plan.n == 0) continue;
+        const int ns = bh[1] >= 0 ? 2 : 1;
+        const int mk[2] = {mat_k_of(p, bh[0]), ns == 2 ? mat_k_of(p, bh[1]) : -1};
+        const bool shared_kv = ns == 2 && mk[0] == mk[1];
+        // ---- Q (both streams) into the pair's slot
+        const int qs = po & 1;
+        ptx::mbar_wait(q_empty + qs, ((po >> 1) & 1) ^ 1);
+        ++po;
+        uint32_t qbytes = C::kQHiBytes + 512 * C::kChHi;
+        if (LOW != kLowHigh) qbytes += C::kQLoBytes + 512 * C::kChLo;
+        ptx::mbar_arrive_expect_tx(q_full + qs, qbytes * ns);
+        for (int x = 0; x < ns; ++x) {
+          uint8_t* qdst = smem + C::oQ + (qs * 2 + x) * C::kQStream;
+          uint8_t* sfq = smem + C::oSfQ + (qs * 2 + x) * C::kSfQ;
+          ptx::tma_load_3d(qdst, &p.tm_q_hi, q_full + qs, 0, qt * C::kBM, bh[x]);
+          ptx::bulk_load(sfq, p.sf_q_hi + (static_cast<int64_t>(bh[x]) * rt_q + qt) * p.ch_hi * 512, 512 * C::kChHi,
+                         q_full + qs);
+          if (LOW != kLowHigh) {
+            ptx::tma_load_3d(qdst + C::kQHiBytes, &p.tm_q_lo, q_full + qs, 0, qt * C::kBM, bh[x]);
+            ptx::bulk_load(sfq + 512 * C::kChHi,
+                           p.sf_q_lo + (static_cast<int64_t>(bh[x]) * rt_q + qt) * p.ch_lo * 512, 512 * C::kChLo,
+                           q_full + qs);
+          }
+        }
+        // ---- per tile: K (+SF +S_q^K) per distinct KV head, then V (+SF)
+        for (int e = 0; e < plan.n; ++e) {
+          int t;
+          bool hi;
+          plan.entry(e, t, hi);
+          if (LOW == kLowHigh) hi = true;
+          const int ch = hi ? C::kChHi : C::kChLo;
+          const uint32_t kbytes = hi ? C::kKBytes : C::kKBytes / 2;
+          const int nk = shared_kv ? 1 : ns;
+          for (int x = 0; x < nk; ++x) {
+            const int ks = kc % C::kNK;
+            ptx::mbar_wait(k_empty + ks, ((kc / C::kNK) & 1) ^ 1);
+            ++kc;
+            // S_q^K for the stream(s) reading this K tile
+            const int s0 = x, s1 = shared_kv ? ns : x + 1;
+            for (int y = s0; y < s1; ++y) {
+              const int sl = sc[y] % C::kNS;
+              ptx::mbar_wait(sq_empty + y * C::kNS + sl, ((sc[y] / C::kNS) & 1) ^ 1);
+            }
+            ptx::mbar_arrive_expect_tx(k_full + ks, kbytes + 512 * ch + 512 * (s1 - s0));
+            ptx::tma_load_3d(smem + C::oK + ks * C::kKBytes, hi ? &p.tm_k_hi : &p.tm_k_lo, k_full + ks, 0,
+                             t * C::kBN, mk[x]);
+            const uint8_t* sfsrc = (hi ? p.sf_k_hi : p.sf_k_lo) +
+                                   (static_cast<int64_t>(mk[x]) * rt_k + t) * (hi ? p.ch_hi : p.ch_lo) * 512;
+            ptx::bulk_load(smem + C::oSfK + ks * 512 * C::kChK, sfsrc, 512 * ch, k_full + ks);
+            for (int y = s0; y < s1; ++y) {
+              const int sl = sc[y] % C::kNS;
+              ++sc[y];
+              ptx::bulk_load(smem + C::oSqK + (y * C::kNS + sl) * 512,
+                             p.qs_k + static_cast<int64_t>(mk[x]) * p.lk_pad + t * C::kBN, 512, k_full + ks);
+            }
+          }
+          for (int x = 0; x < nk; ++x) {
+            const int vs = vc % C::kNV;
+            ptx::mbar_wait(v_empty + vs, ((vc / C::kNV) & 1) ^ 1);
+            ++vc;
+            ptx::mbar_arrive_expect_tx(v_full + vs, C::kVBytes + 512);
+            ptx::tma_load_3d(smem + C::oV + vs * C::kVBytes, &p.tm_v, v_full + vs, 0, t * C::kBN, mk[x]);
+            ptx::bulk_load(smem + C::oSfV + vs * 512, p.sf_v + (static_cast<int64_t>(mk[x]) * rt_k + t) * 512, 512,
+                           v_full + vs);
+          }
+        }
+      }
+      // last CTA out resets the ticket for the next launch (stream-ordered)
+      __threadfence();
+      const unsigned int done = atomicAdd(pp.ticket + 1, 1u);
+      if (done == gridDim.x - 1) {
+        pp.ticket[0] = 0u;
+        pp.ticket[1] = 0u;
+        __threadfence();
+      }
+    }
+  } else if (warp == 1) {
+    // =========================== MMA issuer ===========================
+    if (lane == 0) {
+      ptx::tc_cp_sf(tmem + C::tSfP, ptx::smem_desc(ptx::smem_u32(smem + C::oSfP), 0, 128, ptx::kSwNone));
+      uint32_t kc = 0, vc = 0, su = 0, po = 0, gs[2] = {0, 0}, pv[2] = {0, 0};
+      for (uint32_t i = 0;; ++i) {
+        const int ss = i % C::kNSch;
+        ptx::mbar_wait(sch_full + ss, (i / C::kNSch) & 1);
+        const int k = sched[ss];
+        ptx::mbar_arrive(sch_empty + ss);
+        if (k < 0) break;
+        int bh[2], qt;
+        pair_coords(p, pp, k, bh[0], bh[1], qt);
+        Plan plan;
+        plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
+        if (plan.n == 0) continue;
+        const int ns = bh[1] >= 0 ? 2 : 1;
+        const bool shared_kv = ns == 2 && mat_k_of(p, bh[0]) == mat_k_of(p, bh[1]);
+        const int qs = po & 1;
+        ptx::mbar_wait(q_full + qs, (po >> 1) & 1);
+        ++po;
+        ptx::tc_fence_after();
+        uint32_t kslot[2] = {0, 0}, vslot[2] = {0, 0};
+
+        auto issue_qk = [&](int x, int e) {
+          int t;
+          bool hi;
+          plan.entry(e, t, hi);
+          if (LOW == kLowHigh) hi = true;
+          // the single S buffer: wait until its previous user copied it out
+          ptx::mbar_wait(s_free, (su & 1) ^ 1);
+          ++su;
+          ptx::tc_fence_after();
+          if (e == 0) {
+            const uint8_t* sfq = smem + C::oSfQ + (qs * 2 + x) * C::kSfQ;
+            for (int j = 0; j < C::kChHi; ++j)
+              ptx::tc_cp_sf(tmem + C::tSfQ(x) + 4 * j,
+                            ptx::smem_desc(ptx::smem_u32(sfq + 512 * j), 0, 128, ptx::kSwNone));
+            if (LOW != kLowHigh)
+              for (int j = 0; j < C::kChLo; ++j)
+                ptx::tc_cp_sf(tmem + C::tSfQ(x) + 4 + 4 * j,
+                              ptx::smem_desc(ptx::smem_u32(sfq + 512 * (C::kChHi + j)), 0, 128, ptx::kSwNone));
+          }
+          if (x == 0 || !shared_kv) {
+            kslot[x] = kc % C::kNK;
+            ptx::mbar_wait(k_full + kslot[x], (kc / C::kNK) & 1);
+            ++kc;
+            ptx::tc_fence_after();
+          } else {
+            kslot[1] = kslot[0];
+          }
+          const int ks = kslot[x];
+          const int ch = hi ? C::kChHi : C::kChLo;
+          for (int j = 0; j < ch; ++j)
+            ptx::tc_cp_sf(tmem + C::tSfK(x) + 4 * j,
+                          ptx::smem_desc(ptx::smem_u32(smem + C::oSfK + ks * 512 * C::kChK + 512 * j), 0, 128,
+                                         ptx::kSwNone));
+          const uint32_t kaddr = ptx::smem_u32(smem + C::oK + ks * C::kKBytes);
+          const uint32_t qaddr = ptx::smem_u32(smem + C::oQ + (qs * 2 + x) * C::kQStream);
+          const uint32_t tsfq = tmem + C::tSfQ(x), tsfk = tmem + C::tSfK(x), tSd = tmem + C::tS;
+          if (hi) {
+            constexpr int rb = D;
+            const uint32_t sw = swz_mode(rb);
+            const uint32_t f = static_cast<uint32_t>(p.hfmt);
+#pragma unroll
+            for (int kk = 0; kk < D / 32; ++kk) {
+              const uint64_t ad = ptx::smem_desc(qaddr + 32 * kk, 16, 8 * rb, sw);
+              const uint64_t bd = ptx::smem_desc(kaddr + 32 * kk, 16, 8 * rb, sw);
+              const uint32_t id = ptx::idesc_bs(f, f, 0, 0, 128, 128, 1, kk & 3, kk & 3);
+              ptx::mma_mxf8f6f4(tSd, ad, bd, id, tsfq + 4 * (kk >> 2), tsfk + 4 * (kk >> 2), kk > 0);
+            }
+          } else {
+            const uint32_t qlo = qaddr + C::kQHiBytes;
+            constexpr int rb = D / 2;
+            const uint32_t sw = swz_mode(rb);
+#pragma unroll
+            for (int kk = 0; kk < D / 64; ++kk) {
+              const uint64_t ad = ptx::smem_desc(qlo + 32 * kk, 16, 8 * rb, sw);
+              const uint64_t bd = ptx::smem_desc(kaddr + 32 * kk, 16, 8 * rb, sw);
+              if (LOW == kLowNV) {
+                const uint32_t id = ptx::idesc_bs(1, 1, 0, 0, 128, 128, 0, 0, 0);
+                ptx::mma_nvf4(tSd, ad, bd, id, tsfq + 4 + 4 * kk, tsfk + 4 * kk, kk > 0);
+              } else {
+                const uint32_t sid = (kk & 1) * 2;
+                const uint32_t id = ptx::idesc_bs(1, 1, 0, 0, 128, 128, 1, sid, sid);
+                ptx::mma_mxf4(tSd, ad, bd, id, tsfq + 4 + 4 * (kk >> 1), tsfk + 4 * (kk >> 1), kk > 0);
+              }
+            }
+          }
+          if (x == ns - 1 || !shared_kv) ptx::tc_commit(k_empty + ks);  // last reader of this K slot
+          ptx::tc_commit(s_full + x);
+          ++gs[x];
+          if (e == plan.n - 1 && x == ns - 1) ptx::tc_commit(q_empty + qs);  // Q slot free after these
+        };
+
+        auto issue_pv = [&](int x, int e) {
+          ptx::mbar_wait(p_full + x, pv[x] & 1);
+          ++pv[x];
+          ptx::tc_fence_after();
+          if (x == 0 || !shared_kv) {
+            vslot[x] = vc % C::kNV;
+            ptx::mbar_wait(v_full + vslot[x], (vc / C::kNV) & 1);
+            ++vc;
+            ptx::tc_fence_after();
+          } else {
+            vslot[1] = vslot[0];
+          }
+          const int vs = vslot[x];
+          ptx::tc_cp_sf(tmem + C::tSfV(x),
+                        ptx::smem_desc(ptx::smem_u32(smem + C::oSfV + vs * 512), 0, 128, ptx::kSwNone));
+          const uint32_t vaddr = ptx::smem_u32(smem + C::oV + vs * C::kVBytes);
+          constexpr int rb = DV;  // fp8 V row bytes (MN-major)
+#pragma unroll
+          for (int kk = 0; kk < C::kBN / 32; ++kk) {
+            const uint64_t bd = ptx::smem_desc(vaddr + kk * 32 * rb, 16, 8 * rb, swz_mode(rb));
+            const uint32_t id = ptx::idesc_bs(0, 0, 0, 1, 128, DV, 1, kk & 3, kk & 3);
+            ptx::mma_mxf8f6f4_ts(tmem + C::tO(x), tmem + C::tP(x) + 8 * kk, bd, id, tmem + C::tSfP,
+                                 tmem + C::tSfV(x), !(e == 0 && kk == 0));
+          }
+          if (x == ns - 1 || !shared_kv) ptx::tc_commit(v_empty + vs);
+          ptx::tc_commit(o_done + x);
+        };
+
+        issue_qk(0, 0);
+        if (ns == 2) issue_qk(1, 0);
+        for (int e = 0; e < plan.n; ++e) {
+          if (e + 1 < plan.n) issue_qk(0, e + 1);
+          issue_pv(0, e);
+          if (ns == 2) {
+            if (e + 1 < plan.n) issue_qk(1, e + 1);
+            issue_pv(1, e);
+          }
+        }
+        (void)gs;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // =========================== softmax (one warpgroup per stream) ===========================
+    const int x = (warp - 4) >> 2;  // stream
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;  // query row within the tile == TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+    constexpr float kPShift = 8.f;   // P stored as E4M3(P * 2^8)
+    uint32_t g = 0, sc = 0;          // this stream's tile ordinal / S_q^K ring counter
+
+    for (uint32_t i = 0;; ++i) {
+      const int ss = i % C::kNSch;
+      ptx::mbar_wait(sch_full + ss, (i / C::kNSch) & 1);
+      const int k = sched[ss];
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(sch_empty + ss);
+      if (k < 0) break;
+      int bh[2], qt;
+      pair_coords(p, pp, k, bh[0], bh[1], qt);
+      const int my_bh = bh[x];
+      Plan plan;
+      plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
+      if (my_bh < 0) continue;  // odd head count: stream B idles on this pair
+      const int q0 = qt * C::kBM;
+      const int qrow = q0 + r;
+      const float sq_q = (qrow < p.lq) ? p.qs_q[static_cast<int64_t>(my_bh) * p.lq_pad + qrow] : 1.0f;
+      float m_run = -INFINITY;
+      float2 l2 = make_float2(0.f, 0.f);
+
+      for (int e = 0; e < plan.n; ++e, ++g) {
+        int t;
+        bool hi;
+        plan.entry(e, t, hi);
+        if (LOW == kLowHigh) hi = true;
+        const bool two_level = hi || (LOW == kLowNV);
+        const int k0 = t * C::kBN;
+        ptx::mbar_wait(s_full + x, g & 1);
+        ptx::tc_fence_after();
+        float s[128];
+        {
+          const uint32_t tS = tmem + C::tS + lane_base;
+          uint32_t ra[32], rb2[32], rc[32], rd[32];
+          ptx::tmem_ld32(tS, ra);
+          ptx::tmem_ld32(tS + 32, rb2);
+          ptx::tmem_ld32(tS + 64, rc);
+          ptx::tmem_ld32(tS + 96, rd);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i2 = 0; i2 < 32; ++i2) {
+            s[i2] = __uint_as_float(ra[i2]);
+            s[32 + i2] = __uint_as_float(rb2[i2]);
+            s[64 + i2] = __uint_as_float(rc[i2]);
+            s[96 + i2] = __uint_as_float(rd[i2]);
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(s_free);  // S buffer may be overwritten by the next QK
+        const float rowf = two_level ? sq_q : 1.0f;
+        {
+          const int sl = sc % C::kNS;
+          ++sc;
+          if (two_level) {
+            const float4* sqk = reinterpret_cast<const float4*>(smem + C::oSqK + (x * C::kNS + sl) * 512);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float4 f = sqk[j];
+              const float2 a = __fmul2_rn(make_float2(s[4 * j], s[4 * j + 1]), make_float2(f.x, f.y));
+              const float2 b = __fmul2_rn(make_float2(s[4 * j + 2], s[4 * j + 3]), make_float2(f.z, f.w));
+              s[4 * j] = a.x; s[4 * j + 1] = a.y; s[4 * j + 2] = b.x; s[4 * j + 3] = b.y;
+            }
+          }
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(sq_empty + x * C::kNS + sl);
+        }
+        // causal (attention.py:178-184, applied when k1-1 > q0, :306) and ragged-key masks
+        const int kvalid = p.lk - k0;
+        const bool need_causal = p.causal && (k0 + (kvalid < C::kBN ? kvalid : C::kBN) - 1 > q0);
+        if (need_causal || kvalid < C::kBN) {
+          const int lim = need_causal ? min(qrow - k0 + 1, kvalid) : kvalid;
+#pragma unroll
+          for (int j = 0; j < 128; ++j)
+            if (j >= lim) s[j] = -INFINITY;
+        }
+        float mx = ptx::fmax3(s[0], s[1], s[2]);
+#pragma unroll
+        for (int j = 3; j < 127; j += 2) mx = ptx::fmax3(mx, s[j], s[j + 1]);
+        mx = fmaxf(mx, s[127]);
+        const float m_tile = mx * rowf;
+        const float m_new = fmaxf(m_run, m_tile);
+        const bool dead = (m_new == -INFINITY);
+        const float alpha = dead ? 1.0f : fast_exp2(m_run - m_new);  // m_run = -inf -> 0
+        const float bias = dead ? 0.f : (kPShift - m_new);
+        const float2 rf2 = make_float2(rowf, rowf), b2 = make_float2(bias, bias);
+        // P_x (and O_x) are read by PV(e-1): wait for it before overwriting
+        if (e > 0) {
+          ptx::mbar_wait(o_done + x, (g - 1) & 1);
+          ptx::tc_fence_after();
+        }
+        float2 ls = make_float2(0.f, 0.f);
+        const uint32_t tP = tmem + C::tP(x) + lane_base;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int b0 = 32 * c + 4 * j;
+            float2 x0 = __ffma2_rn(make_float2(s[b0], s[b0 + 1]), rf2, b2);
+            float2 x1 = __ffma2_rn(make_float2(s[b0 + 2], s[b0 + 3]), rf2, b2);
+            x0.x = fast_exp2(x0.x);
+            x0.y = fast_exp2(x0.y);
+            x1.x = fast_exp2(x1.x);
+            x1.y = fast_exp2(x1.y);
+            ls = __fadd2_rn(ls, __fadd2_rn(x0, x1));
+            pk[j] = static_cast<uint32_t>(ptx::cvt_e4m3x2(x0.x, x0.y)) |
+                    (static_cast<uint32_t>(ptx::cvt_e4m3x2(x1.x, x1.y)) << 16);
+          }
+          ptx::tmem_st8(tP + 8 * c, pk);
+        }
+        l2 = __ffma2_rn(l2, make_float2(alpha, alpha), ls);
+        m_run = m_new;
+        if (e > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+          const uint32_t tO = tmem + C::tO(x) + lane_base;
+          const float2 a2 = make_float2(alpha, alpha);
+#pragma unroll
+          for (int c = 0; c < DV / 32; ++c) {
+            uint32_t rr[32];
+            ptx::tmem_ld32(tO + 32 * c, rr);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i2 = 0; i2 < 16; ++i2) {
+              const float2 v = __fmul2_rn(make_float2(__uint_as_float(rr[2 * i2]), __uint_as_float(rr[2 * i2 + 1])), a2);
+              rr[2 * i2] = __float_as_uint(v.x);
+              rr[2 * i2 + 1] = __float_as_uint(v.y);
+            }
+            ptx::tmem_st32(tO + 32 * c, rr);
+          }
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(p_full + x);
+      }
+
+      // ---- epilogue: O / l (attention.py:104-106)
+      const float l_run = l2.x + l2.y;
+      const float inv_l = 1.0f / (l_run > 0.f ? l_run : 1.0f);
+      if (plan.n > 0) {
+        ptx::mbar_wait(o_done + x, (g - 1) & 1);
+        ptx::tc_fence_after();
+      }
+      const uint32_t tO = tmem + C::tO(x) + lane_base;
+      const int64_t orow = static_cast<int64_t>(my_bh) * p.lq + qrow;
+#pragma unroll
+      for (int c = 0; c < DV / 32; ++c) {
+        uint32_t rr[32];
+        if (plan.n > 0) {
+          ptx::tmem_ld32(tO + 32 * c, rr);
+          ptx::tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i2 = 0; i2 < 32; ++i2) rr[i2] = 0u;
+        }
+        if (qrow < p.lq) {
+          if (p.out_bf16) {
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o) + orow * DV + 32 * c);
+#pragma unroll
+            for (int i2 = 0; i2 < 4; ++i2) {
+              uint32_t wv[4];
+#pragma unroll
+              for (int k2 = 0; k2 < 4; ++k2) {
+                __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(rr[8 * i2 + 2 * k2]) * inv_l,
+                                                         __uint_as_float(rr[8 * i2 + 2 * k2 + 1]) * inv_l);
+                wv[k2] = *reinterpret_cast<uint32_t*>(&v);
+              }
+              dst[i2] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            }
+          } else {
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.o) + orow * DV + 32 * c);
+#pragma unroll
+            for (int i2 = 0; i2 < 8; ++i2)
+              dst[i2] = make_float4(__uint_as_float(rr[4 * i2]) * inv_l, __uint_as_float(rr[4 * i2 + 1]) * inv_l,
+                                    __uint_as_float(rr[4 * i2 + 2]) * inv_l, __uint_as_float(rr[4 * i2 + 3]) * inv_l);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc<512>(tmem);
+}
+
+}  // namespace dma

@@ -3,10 +3,12 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "attn.cuh"
+#include "attn_pp.cuh"
 #include "common.cuh"
 #include "quant.cuh"
 
@@ -66,7 +68,7 @@ struct Layout {
   bool low_fp4, pv_bf16, v_convert, tensor_gran;
   // byte offsets
   size_t q_hi, q_lo, k_hi, k_lo, v_codes, v_bf16;  // large buffers
-  size_t small_begin, sf_q_hi, sf_q_lo, sf_k_hi, sf_k_lo, sf_v, qs_q, qs_k, small_end;
+  size_t small_begin, sf_q_hi, sf_q_lo, sf_k_hi, sf_k_lo, sf_v, qs_q, qs_k, ticket, small_end;
   size_t absmax_q, absmax_k, total;
 };
 
@@ -105,6 +107,7 @@ static Layout plan_layout(const DmaAttnArgs* a) {
   L.sf_v = L.pv_bf16 ? 0 : take(L.mk * (L.lk_pad / 128) * ((DV + 127) / 128) * 512);
   L.qs_q = take(L.mq * L.lq_pad * 4);
   L.qs_k = take(L.mk * L.lk_pad * 4);
+  L.ticket = take(64);  // dynamic pair scheduler ticket (zeroed with the small region; self-resetting)
   L.small_end = off;
   L.absmax_q = L.tensor_gran ? take(L.mq * 8) : 0;
   L.absmax_k = L.tensor_gran ? take(L.mk * 8) : 0;
@@ -157,7 +160,6 @@ __global__ void to_bf16_kernel(const void* src, int dt, int64_t n, __nv_bfloat16
   }
 }
 
-static int elem_bytes(int dt) { return dt == DMA_DT_F64 ? 8 : (dt == DMA_DT_F32 ? 4 : 2); }
 
 int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStream_t st) {
   const int64_t D = a->head_dim, DV = a->v_dim;
@@ -222,6 +224,16 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
   return 0;
 }
 
+// DMA_SINGLE_STREAM=1 selects the one-stream kernel for the MXFP8 PV path too (A/B comparisons)
+static bool force_single_stream() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DMA_SINGLE_STREAM");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -242,6 +254,19 @@ static int launch_attn(const AttnParams& p, int64_t items, cudaStream_t st) {
   // persistent: one CTA per SM, items strided across CTAs (longest first)
   const int64_t grid = items < num_sms() ? items : num_sms();
   kern<<<static_cast<unsigned>(grid), 384, smem, st>>>(p);
+  DMA_LAUNCH_CHECK();
+  ++g_launches;
+  return 0;
+}
+
+template <int D, int LOW>
+static int launch_pp(const AttnParams& p, const PPParams& q, cudaStream_t st) {
+  using C = PPCfg<D, D, LOW>;
+  auto kern = dma_attn_pp_kernel<D, D, LOW>;
+  static_assert(C::kSmemBytes <= 227 * 1024, "smem budget");
+  DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+  const int grid = q.n_pairs < num_sms() ? q.n_pairs : num_sms();
+  kern<<<static_cast<unsigned>(grid), 384, C::kSmemBytes, st>>>(p, q);
   DMA_LAUNCH_CHECK();
   ++g_launches;
   return 0;
@@ -301,6 +326,18 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
   p.n_bh = static_cast<int>(L.mq);
   p.n_items = static_cast<int>(items);
   const int low = a->low_format == DMA_FMT_NVFP4 ? kLowNV : (a->low_format == DMA_FMT_MXFP4 ? kLowMX4 : kLowHigh);
+  if (!L.pv_bf16 && !force_single_stream()) {
+    // ping-pong kernel (block-scaled MXFP8 PV): pairs of heads share one query-tile plan
+    PPParams q{};
+    q.pairs_per_qt = static_cast<int>((L.mq + 1) / 2);
+    q.n_pairs = q.pairs_per_qt * p.n_qt;
+    const double kv_bytes = static_cast<double>(L.mk) * static_cast<double>(L.lk_pad) * (2.6 * static_cast<double>(D));
+    q.head_major = kv_bytes > 48.0 * 1024 * 1024;  // K/V exceed ~L2/2: keep all CTAs on the same heads
+    q.ticket = reinterpret_cast<unsigned int*>(ws + L.ticket);
+    if (low == kLowNV) return D == 64 ? launch_pp<64, kLowNV>(p, q, st) : launch_pp<128, kLowNV>(p, q, st);
+    if (low == kLowMX4) return D == 64 ? launch_pp<64, kLowMX4>(p, q, st) : launch_pp<128, kLowMX4>(p, q, st);
+    return D == 64 ? launch_pp<64, kLowHigh>(p, q, st) : launch_pp<128, kLowHigh>(p, q, st);
+  }
   return D == 64 ? dispatch_attn<64>(p, low, L.pv_bf16, items, st) : dispatch_attn<128>(p, low, L.pv_bf16, items, st);
 }
 
