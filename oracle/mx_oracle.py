@@ -449,10 +449,16 @@ def quantize_v_keys(v: np.ndarray) -> np.ndarray:
     return deq.reshape(-1, dv)[:n]
 
 
+# The MXFP8-PV kernel (attn_pp.cuh) keeps a row's running max until a tile raises
+# it by more than LAZY_RESCALE (log2 units) and stores P as E4M3(P * 2^(8 - LAZY)).
+LAZY_RESCALE = {"mxfp8": 4.0}
+
+
 def _quantize_p(p: np.ndarray, pv: str) -> np.ndarray:
-    """P as the kernel feeds it to the PV contraction: E4M3(P * 2^8) * 2^-8, or bf16 (RNE)."""
+    """P as the kernel feeds it to the PV contraction: E4M3(P * 2^s) * 2^-s, or bf16 (RNE)."""
     if pv == "mxfp8":
-        return decode_fp8(encode_fp8(p * 256.0, E4M3), E4M3) / 256.0
+        sc = 2.0 ** (8.0 - LAZY_RESCALE["mxfp8"])
+        return decode_fp8(encode_fp8(p * sc, E4M3), E4M3) / sc
     if pv == "bf16":
         b = p.astype(np.float32).view(np.uint32).astype(np.uint64)
         b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
@@ -464,10 +470,12 @@ def mixed_precision_attention(q, k, v, cfg: Cfg, pv: str = "f64") -> np.ndarray:
     """Tile loop + base-2 online softmax (attention.py:150-175, 178-184, 282-310).
 
     ``pv="f64"`` is the reference exactly.  ``pv="mxfp8"`` / ``"bf16"`` add the
-    sm_100a kernel's stated PV quantization (P -> E4M3 x 2^8 with V -> MXFP8
-    along keys, or P and V in bf16) on top of the same algorithm; the row sum
-    l still uses the unquantized P, as the kernel does.  Test infrastructure only.
+    sm_100a kernel's stated PV quantization (P -> E4M3 x 2^4 with V -> MXFP8
+    along keys and lazy max rescaling, or P and V in bf16) on top of the same
+    algorithm; the row sum l still uses the unquantized P, as the kernel does.
+    Test infrastructure only.
     """
+    lazy = LAZY_RESCALE.get(pv, 0.0)
     ql, qh, kl, kh, v = operands(q, k, v, cfg)
     if pv == "mxfp8":
         v = quantize_v_keys(v)
@@ -489,6 +497,8 @@ def mixed_precision_attention(q, k, v, cfg: Cfg, pv: str = "f64") -> np.ndarray:
                 kj = np.arange(k0, k1)[None, :]
                 s = np.where(qi >= kj, s, -np.inf)
             m_new = np.maximum(m, s.max(axis=1))
+            if lazy:
+                m_new = np.where(m_new > m + lazy, m_new, m)
             alive = np.isfinite(m_new)
             alpha = np.where(alive, np.exp2(np.where(alive, m - m_new, 0.0)), 1.0)
             p = np.zeros_like(s)

@@ -144,7 +144,7 @@ template <int D, int DV, int LOW, bool PVBF16>
 __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant__ AttnParams p) {
   using C = AttnCfg<D, DV, LOW, PVBF16>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::oBar);
   uint64_t* q_full = bars + 0;                // [kNQ]
   uint64_t* q_empty = q_full + C::kNQ;        // [kNQ]
@@ -457,10 +457,10 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
         // S_q^K column factors for two-level tiles (staged by the producer with the K tile)
         const float rowf = two_level ? sq_q : 1.0f;
         if (two_level) {
-          const float4* sqk = reinterpret_cast<const float4*>(smem + C::oSqK + ((g % C::kNK) * 512)) + 16 * half;
+          const uint32_t sqk = ptx::smem_u32(smem + C::oSqK + ((g % C::kNK) * 512)) + 256 * half;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const float4 f = sqk[j];
+            const float4 f = ptx::lds_f4(sqk + 16 * j);
             float2 a = __fmul2_rn(make_float2(s[4 * j], s[4 * j + 1]), make_float2(f.x, f.y));
             float2 b = __fmul2_rn(make_float2(s[4 * j + 2], s[4 * j + 3]), make_float2(f.z, f.w));
             s[4 * j] = a.x; s[4 * j + 1] = a.y; s[4 * j + 2] = b.x; s[4 * j + 3] = b.y;

@@ -20,8 +20,10 @@
 // The MMA issuer runs QK_A(0) QK_B(0) { QK_A(j+1) PV_A(j) QK_B(j+1) PV_B(j) }:
 // a QK waits until the previous S consumer has copied S into registers.
 //
-// Warps: 0 producer (TMA + scheduler), 1 MMA issuer, 2-3 idle,
-//        4-7 softmax stream A, 8-11 softmax stream B (one query row per thread).
+// Warps: 0-3 softmax stream A, 4-7 softmax stream B, 8 producer (TMA +
+//        scheduler), 9 MMA issuer, 10-11 idle.  setmaxnreg moves registers from
+//        warpgroup 2 (72 each) to the softmax warpgroups (216 each), whose
+//        128-value S fragment stays in registers.
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -32,6 +34,34 @@
 #include "ptx.cuh"
 
 namespace dma {
+
+// Optional phase timers (-DDMA_PROFILE): per-role cycle counters summed over
+// all warps into g_prof (read back with dma_prof_read).  Off in normal builds.
+#ifdef DMA_PROFILE
+__device__ unsigned long long g_prof[32];
+#define PROF_DECL unsigned long long prof_acc[16] = {0}; long long prof_t = clock64();
+#define PROF_MARK(i)                       \
+  do {                                     \
+    const long long _t = clock64();        \
+    prof_acc[i] += (unsigned long long)(_t - prof_t); \
+    prof_t = _t;                           \
+  } while (0)
+#define PROF_FLUSH(base, n)                                          \
+  do {                                                               \
+    if ((threadIdx.x & 31) == 0)                                     \
+      for (int _i = 0; _i < (n); ++_i) atomicAdd(&g_prof[(base) + _i], prof_acc[_i]); \
+  } while (0)
+#else
+#define PROF_DECL
+#define PROF_MARK(i) do {} while (0)
+#define PROF_FLUSH(base, n) do {} while (0)
+#endif
+
+#ifndef DMA_PP_TURNS
+#define DMA_PP_TURNS 0
+#endif
+// 1: the two softmax warpgroups take strict turns for their exp2 phases
+constexpr bool kTurns = DMA_PP_TURNS != 0;
 
 struct PPParams {
   int n_pairs;
@@ -99,7 +129,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
                                                              const __grid_constant__ PPParams pp) {
   using C = PPCfg<D, DV, LOW>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::oBar);
   uint64_t* q_full = bars;                        // [2]
   uint64_t* q_empty = q_full + 2;                 // [2]
@@ -120,7 +150,8 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rt_q = p.lq_pad >> 7, rt_k = p.lk_pad >> 7;
 
-  if (warp == 0) {
+  constexpr int kProducer = 8, kMma = 9;  // warps 0-7: softmax (stream = warp / 4)
+  if (warp == kProducer) {
     if (lane == 0) {
       for (int i = 0; i < 2; ++i) {
         ptx::mbar_init(q_full + i, 1);
@@ -152,9 +183,9 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
         ptx::tma_prefetch_desc(&p.tm_k_lo);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMma) {
     ptx::tmem_alloc<512>(tmem_slot);
-  } else if (warp == 2) {
+  } else if (warp == 0) {
     // constant P scale-factor atom: E8M0 127 (= 1.0) for every row / k-block
     uint32_t* sfp = reinterpret_cast<uint32_t*>(smem + C::oSfP);
     for (int i = lane; i < 128; i += 32) sfp[i] = 0x7F7F7F7Fu;
@@ -165,7 +196,10 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp >= 8) {
+  // register budget: warpgroup 2 gives registers to the softmax warpgroups
+  ptx::setmaxnreg_dec<72>();
+  if (warp == kProducer) {
     // =========================== scheduler + TMA producer ===========================
     if (lane == 0) {
       uint32_t kc = 0, vc = 0, sc[2] = {0, 0}, po = 0;
@@ -257,7 +291,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
         __threadfence();
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMma) {
     // =========================== MMA issuer ===========================
     if (lane == 0) {
       ptx::tc_cp_sf(tmem + C::tSfP, ptx::smem_desc(ptx::smem_u32(smem + C::oSfP), 0, 128, ptx::kSwNone));
@@ -394,18 +428,33 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
+  }
+  } else {
+    ptx::setmaxnreg_inc<216>();  // the 128-value S fragment stays in registers
     // =========================== softmax (one warpgroup per stream) ===========================
-    const int x = (warp - 4) >> 2;  // stream
+    // TMEM is read in the 16x256b shape: thread (r0 = lane/4, m = lane%4) of a warp
+    // holds rows quad*32 + r0 + 8i (i = 0..3) and the 32 S columns 8g + 2m + b.
+    // K rows are permuted inside every 128-key tile (quant.cuh, kPermKeys) so that
+    // these 32 columns are exactly the keys 32g' + 8m + (0..7) whose E4M3 P bytes
+    // form the P words this thread owns in the same shape: no shuffles for P,
+    // and only 32 (not 128) S_q^K factors per thread per tile.
+    const int x = warp >> 2;  // stream
     const int quad = warp & 3;
-    const int r = quad * 32 + lane;  // query row within the tile == TMEM lane
+    const int m4 = lane & 3, r0 = lane >> 2;
     const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
-    constexpr float kPShift = 8.f;   // P stored as E4M3(P * 2^8)
-    uint32_t g = 0, sc = 0;          // this stream's tile ordinal / S_q^K ring counter
+    constexpr uint32_t kHalf = 16u << 16;  // lane offset of the second 16-lane block
+    // Lazy rescaling (the FA4 trick): a row keeps its running max until a tile
+    // raises it by more than kLazy (log2 units), so O is rarely rescaled.  P can
+    // then reach 2^kLazy and is stored as E4M3(P * 2^(8 - kLazy)) <= 256 < 448.
+    constexpr float kLazy = 4.f;
+    constexpr float kPShift = 8.f - kLazy;
+    uint32_t g = 0, sc = 0;                // this stream's tile ordinal / S_q^K ring counter
+    if (kTurns && x == 1) ptx::named_bar_arrive(1, 256);  // A takes the first exp phase
+    PROF_DECL
 
-    for (uint32_t i = 0;; ++i) {
-      const int ss = i % C::kNSch;
-      ptx::mbar_wait(sch_full + ss, (i / C::kNSch) & 1);
+    for (uint32_t it = 0;; ++it) {
+      const int ss = it % C::kNSch;
+      ptx::mbar_wait(sch_full + ss, (it / C::kNSch) & 1);
       const int k = sched[ss];
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(sch_empty + ss);
@@ -416,11 +465,17 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
       Plan plan;
       plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
       if (my_bh < 0) continue;  // odd head count: stream B idles on this pair
+      const bool pair2 = bh[1] >= 0;
       const int q0 = qt * C::kBM;
-      const int qrow = q0 + r;
-      const float sq_q = (qrow < p.lq) ? p.qs_q[static_cast<int64_t>(my_bh) * p.lq_pad + qrow] : 1.0f;
-      float m_run = -INFINITY;
-      float2 l2 = make_float2(0.f, 0.f);
+      int qrow[4];
+      float sq_q[4], m_run[4], l_run[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        qrow[i] = q0 + quad * 32 + r0 + 8 * i;
+        sq_q[i] = (qrow[i] < p.lq) ? p.qs_q[static_cast<int64_t>(my_bh) * p.lq_pad + qrow[i]] : 1.0f;
+        m_run[i] = -INFINITY;
+        l_run[i] = 0.f;
+      }
 
       for (int e = 0; e < plan.n; ++e, ++g) {
         int t;
@@ -429,123 +484,172 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
         if (LOW == kLowHigh) hi = true;
         const bool two_level = hi || (LOW == kLowNV);
         const int k0 = t * C::kBN;
+        PROF_MARK(9);
         ptx::mbar_wait(s_full + x, g & 1);
         ptx::tc_fence_after();
+        PROF_MARK(0);
+        // S fragment, loaded in place: s[64 (i / 2) + 4 g + 2 (i % 2) + b] = S[row i][col 8g + 2m + b]
         float s[128];
-        {
-          const uint32_t tS = tmem + C::tS + lane_base;
-          uint32_t ra[32], rb2[32], rc[32], rd[32];
-          ptx::tmem_ld32(tS, ra);
-          ptx::tmem_ld32(tS + 32, rb2);
-          ptx::tmem_ld32(tS + 64, rc);
-          ptx::tmem_ld32(tS + 96, rd);
-          ptx::tmem_ld_wait();
-#pragma unroll
-          for (int i2 = 0; i2 < 32; ++i2) {
-            s[i2] = __uint_as_float(ra[i2]);
-            s[32 + i2] = __uint_as_float(rb2[i2]);
-            s[64 + i2] = __uint_as_float(rc[i2]);
-            s[96 + i2] = __uint_as_float(rd[i2]);
-          }
-        }
+        ptx::tmem_ld_16x256b_x16(tmem + C::tS + lane_base, *reinterpret_cast<uint32_t(*)[64]>(&s[0]));
+        ptx::tmem_ld_16x256b_x16(tmem + C::tS + lane_base + kHalf, *reinterpret_cast<uint32_t(*)[64]>(&s[64]));
+        ptx::tmem_ld_wait();
+#define SIDX(i, gg, b) (64 * ((i) >> 1) + 4 * (gg) + 2 * ((i) & 1) + (b))
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(s_free);  // S buffer may be overwritten by the next QK
-        const float rowf = two_level ? sq_q : 1.0f;
+        PROF_MARK(1);
         {
           const int sl = sc % C::kNS;
           ++sc;
           if (two_level) {
-            const float4* sqk = reinterpret_cast<const float4*>(smem + C::oSqK + (x * C::kNS + sl) * 512);
+            // this thread's 32 factors are contiguous: [32 m + 2 g + b]
+            const uint32_t sqk = ptx::smem_u32(smem + C::oSqK + (x * C::kNS + sl) * 512) + 128 * m4;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float4 f = sqk[j];
-              const float2 a = __fmul2_rn(make_float2(s[4 * j], s[4 * j + 1]), make_float2(f.x, f.y));
-              const float2 b = __fmul2_rn(make_float2(s[4 * j + 2], s[4 * j + 3]), make_float2(f.z, f.w));
-              s[4 * j] = a.x; s[4 * j + 1] = a.y; s[4 * j + 2] = b.x; s[4 * j + 3] = b.y;
+            for (int j = 0; j < 8; ++j) {  // factors for columns g = 2j, 2j + 1
+              const float4 f = ptx::lds_f4(sqk + 16 * j);
+              const float2 f0 = make_float2(f.x, f.y), f1 = make_float2(f.z, f.w);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 a = __fmul2_rn(make_float2(s[SIDX(i, 2 * j, 0)], s[SIDX(i, 2 * j, 1)]), f0);
+                const float2 b = __fmul2_rn(make_float2(s[SIDX(i, 2 * j + 1, 0)], s[SIDX(i, 2 * j + 1, 1)]), f1);
+                s[SIDX(i, 2 * j, 0)] = a.x;
+                s[SIDX(i, 2 * j, 1)] = a.y;
+                s[SIDX(i, 2 * j + 1, 0)] = b.x;
+                s[SIDX(i, 2 * j + 1, 1)] = b.y;
+              }
             }
           }
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(sq_empty + x * C::kNS + sl);
         }
-        // causal (attention.py:178-184, applied when k1-1 > q0, :306) and ragged-key masks
+        PROF_MARK(2);
+        // causal (attention.py:178-184, applied when k1-1 > q0, :306) and ragged-key masks;
+        // column 8g + 2m + b holds key k0 + 32(g/4) + 8m + 2(g%4) + b
         const int kvalid = p.lk - k0;
         const bool need_causal = p.causal && (k0 + (kvalid < C::kBN ? kvalid : C::kBN) - 1 > q0);
         if (need_causal || kvalid < C::kBN) {
-          const int lim = need_causal ? min(qrow - k0 + 1, kvalid) : kvalid;
 #pragma unroll
-          for (int j = 0; j < 128; ++j)
-            if (j >= lim) s[j] = -INFINITY;
+          for (int i = 0; i < 4; ++i) {
+            const int lim = need_causal ? min(qrow[i] - k0 + 1, kvalid) : kvalid;
+#pragma unroll
+            for (int gg = 0; gg < 16; ++gg)
+#pragma unroll
+              for (int b = 0; b < 2; ++b)
+                if (32 * (gg >> 2) + 8 * m4 + 2 * (gg & 3) + b >= lim) s[SIDX(i, gg, b)] = -INFINITY;
+          }
         }
-        float mx = ptx::fmax3(s[0], s[1], s[2]);
+        float rowf[4], bias[4], alpha[4];
+        bool any_alpha = false;
 #pragma unroll
-        for (int j = 3; j < 127; j += 2) mx = ptx::fmax3(mx, s[j], s[j + 1]);
-        mx = fmaxf(mx, s[127]);
-        const float m_tile = mx * rowf;
-        const float m_new = fmaxf(m_run, m_tile);
-        const bool dead = (m_new == -INFINITY);
-        const float alpha = dead ? 1.0f : fast_exp2(m_run - m_new);  // m_run = -inf -> 0
-        const float bias = dead ? 0.f : (kPShift - m_new);
-        const float2 rf2 = make_float2(rowf, rowf), b2 = make_float2(bias, bias);
+        for (int i = 0; i < 4; ++i) {
+          float mx = fmaxf(s[SIDX(i, 0, 0)], s[SIDX(i, 0, 1)]);
+#pragma unroll
+          for (int gg = 1; gg < 16; ++gg) mx = ptx::fmax3(mx, s[SIDX(i, gg, 0)], s[SIDX(i, gg, 1)]);
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+          rowf[i] = two_level ? sq_q[i] : 1.0f;
+          const float m_cand = fmaxf(m_run[i], mx * rowf[i]);
+          const bool upd = m_cand > m_run[i] + kLazy;  // always for the first live tile (m_run = -inf)
+          const float m_new = upd ? m_cand : m_run[i];
+          const bool dead = (m_new == -INFINITY);
+          alpha[i] = (dead || !upd) ? 1.0f : fast_exp2(m_run[i] - m_new);  // m_run = -inf -> 0
+          bias[i] = dead ? 0.f : (kPShift - m_new);
+          m_run[i] = m_new;
+          any_alpha |= alpha[i] != 1.0f;
+        }
+        PROF_MARK(3);
         // P_x (and O_x) are read by PV(e-1): wait for it before overwriting
         if (e > 0) {
           ptx::mbar_wait(o_done + x, (g - 1) & 1);
           ptx::tc_fence_after();
         }
-        float2 ls = make_float2(0.f, 0.f);
-        const uint32_t tP = tmem + C::tP(x) + lane_base;
+        PROF_MARK(4);
+        // exp phases of the two streams alternate (A, B, A, B, ...): MUFU.EX2 is the
+        // shared bottleneck; each stream's loads / max / O rescale run during the
+        // other's exp phase (named barriers 1 = "A may exp", 2 = "B may exp")
+        if (kTurns && pair2) ptx::named_bar_sync(1 + x, 256);
+        PROF_MARK(5);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[8];
+        for (int blk = 0; blk < 2; ++blk) {  // rows 2 blk, 2 blk + 1 (one 16-lane TMEM block)
+          uint32_t pk[16];  // st.16x256b.x4: rep G -> {row 2blk: word 8G+2m, 8G+2m+1; row 2blk+1: same}
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int b0 = 32 * c + 4 * j;
-            float2 x0 = __ffma2_rn(make_float2(s[b0], s[b0 + 1]), rf2, b2);
-            float2 x1 = __ffma2_rn(make_float2(s[b0 + 2], s[b0 + 3]), rf2, b2);
-            x0.x = fast_exp2(x0.x);
-            x0.y = fast_exp2(x0.y);
-            x1.x = fast_exp2(x1.x);
-            x1.y = fast_exp2(x1.y);
-            ls = __fadd2_rn(ls, __fadd2_rn(x0, x1));
-            pk[j] = static_cast<uint32_t>(ptx::cvt_e4m3x2(x0.x, x0.y)) |
-                    (static_cast<uint32_t>(ptx::cvt_e4m3x2(x1.x, x1.y)) << 16);
-          }
-          ptx::tmem_st8(tP + 8 * c, pk);
-        }
-        l2 = __ffma2_rn(l2, make_float2(alpha, alpha), ls);
-        m_run = m_new;
-        if (e > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
-          const uint32_t tO = tmem + C::tO(x) + lane_base;
-          const float2 a2 = make_float2(alpha, alpha);
+          for (int ii = 0; ii < 2; ++ii) {
+            const int i = 2 * blk + ii;
+            const float2 rf2 = make_float2(rowf[i], rowf[i]), b2 = make_float2(bias[i], bias[i]);
+            float2 ls = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int c = 0; c < DV / 32; ++c) {
-            uint32_t rr[32];
-            ptx::tmem_ld32(tO + 32 * c, rr);
-            ptx::tmem_ld_wait();
+            for (int G = 0; G < 4; ++G) {
 #pragma unroll
-            for (int i2 = 0; i2 < 16; ++i2) {
-              const float2 v = __fmul2_rn(make_float2(__uint_as_float(rr[2 * i2]), __uint_as_float(rr[2 * i2 + 1])), a2);
-              rr[2 * i2] = __float_as_uint(v.x);
-              rr[2 * i2 + 1] = __float_as_uint(v.y);
+              for (int h = 0; h < 2; ++h) {  // word h of rep G = keys of columns g = 4G + 2h, 4G + 2h + 1
+                const int gg = 4 * G + 2 * h;
+                float2 x0 = __ffma2_rn(make_float2(s[SIDX(i, gg, 0)], s[SIDX(i, gg, 1)]), rf2, b2);
+                float2 x1 = __ffma2_rn(make_float2(s[SIDX(i, gg + 1, 0)], s[SIDX(i, gg + 1, 1)]), rf2, b2);
+                x0.x = fast_exp2(x0.x);
+                x0.y = fast_exp2(x0.y);
+                x1.x = fast_exp2(x1.x);
+                x1.y = fast_exp2(x1.y);
+                ls = __fadd2_rn(ls, __fadd2_rn(x0, x1));
+                pk[4 * G + 2 * ii + h] = static_cast<uint32_t>(ptx::cvt_e4m3x2(x0.x, x0.y)) |
+                                         (static_cast<uint32_t>(ptx::cvt_e4m3x2(x1.x, x1.y)) << 16);
+              }
             }
-            ptx::tmem_st32(tO + 32 * c, rr);
+            l_run[i] = fmaf(l_run[i], alpha[i], ls.x + ls.y);
+          }
+          ptx::tmem_st_16x256b_x4(tmem + C::tP(x) + lane_base + (blk ? kHalf : 0u), pk);
+        }
+#undef SIDX
+        if (kTurns && pair2) ptx::named_bar_arrive(2 - x, 256);
+        PROF_MARK(6);
+        if (e > 0 && __any_sync(0xffffffffu, any_alpha)) {
+          // O rows (same 16x256b ownership as S / P) *= alpha
+#pragma unroll
+          for (int blk = 0; blk < 2; ++blk) {
+            const float2 a0 = make_float2(alpha[2 * blk], alpha[2 * blk]);
+            const float2 a1 = make_float2(alpha[2 * blk + 1], alpha[2 * blk + 1]);
+#pragma unroll
+            for (int cq = 0; cq < DV / 32; ++cq) {
+              const uint32_t ta = tmem + C::tO(x) + lane_base + (blk ? kHalf : 0u) + 32 * cq;
+              uint32_t rr[16];
+              ptx::tmem_ld_16x256b_x4(ta, rr);
+              ptx::tmem_ld_wait();
+#pragma unroll
+              for (int G = 0; G < 4; ++G) {
+                const float2 u = __fmul2_rn(make_float2(__uint_as_float(rr[4 * G]), __uint_as_float(rr[4 * G + 1])), a0);
+                const float2 v = __fmul2_rn(make_float2(__uint_as_float(rr[4 * G + 2]), __uint_as_float(rr[4 * G + 3])), a1);
+                rr[4 * G] = __float_as_uint(u.x);
+                rr[4 * G + 1] = __float_as_uint(u.y);
+                rr[4 * G + 2] = __float_as_uint(v.x);
+                rr[4 * G + 3] = __float_as_uint(v.y);
+              }
+              ptx::tmem_st_16x256b_x4(ta, rr);
+            }
           }
         }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(p_full + x);
+        PROF_MARK(7);
       }
 
-      // ---- epilogue: O / l (attention.py:104-106)
-      const float l_run = l2.x + l2.y;
-      const float inv_l = 1.0f / (l_run > 0.f ? l_run : 1.0f);
+      // ---- epilogue: O / l (attention.py:104-106), one row per thread (32x32b)
+      float my_l = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float l = l_run[i];
+        l += __shfl_xor_sync(0xffffffffu, l, 1);
+        l += __shfl_xor_sync(0xffffffffu, l, 2);
+        const float v = __shfl_sync(0xffffffffu, l, 4 * (lane & 7));  // row (lane & 7) + 8 i
+        if ((lane >> 3) == i) my_l = v;
+      }
+      const float inv_l = 1.0f / (my_l > 0.f ? my_l : 1.0f);
       if (plan.n > 0) {
         ptx::mbar_wait(o_done + x, (g - 1) & 1);
         ptx::tc_fence_after();
       }
+      const int orow_q = q0 + quad * 32 + lane;
       const uint32_t tO = tmem + C::tO(x) + lane_base;
-      const int64_t orow = static_cast<int64_t>(my_bh) * p.lq + qrow;
+      const int64_t orow = static_cast<int64_t>(my_bh) * p.lq + orow_q;
 #pragma unroll
       for (int c = 0; c < DV / 32; ++c) {
         uint32_t rr[32];
@@ -556,7 +660,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
 #pragma unroll
           for (int i2 = 0; i2 < 32; ++i2) rr[i2] = 0u;
         }
-        if (qrow < p.lq) {
+        if (orow_q < p.lq) {
           if (p.out_bf16) {
             uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o) + orow * DV + 32 * c);
 #pragma unroll
@@ -580,12 +684,15 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
         }
       }
       ptx::tc_fence_before();
+      PROF_MARK(8);
     }
+    if (kTurns && x == 0) ptx::named_bar_sync(1, 256);  // consume B's last hand-over
+    PROF_FLUSH(0, 10);
   }
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) ptx::tmem_dealloc<512>(tmem);
+  if (warp == kMma) ptx::tmem_dealloc<512>(tmem);
 }
 
 }  // namespace dma

@@ -15,7 +15,7 @@
 namespace dma {
 
 int quantize_impl(const DmaQuantArgs* a, uint8_t* sf_low_op, uint8_t* sf_high_op, float* qs_f32, int64_t rows_pad,
-                  cudaStream_t st);
+                  cudaStream_t st, int key_perm);
 
 static thread_local int g_launches = 0;
 
@@ -62,10 +62,20 @@ static int make_map(CUtensorMap* m, const void* base, CUtensorMapDataType dt, in
   return 0;
 }
 
+// DMA_SINGLE_STREAM=1 selects the one-stream kernel for the MXFP8 PV path too (A/B comparisons)
+static bool force_single_stream() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DMA_SINGLE_STREAM");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // ------------------------------------------------------------ workspace layout
 struct Layout {
   int64_t mq, mk, lq_pad, lk_pad, ch_hi, ch_lo;
-  bool low_fp4, pv_bf16, v_convert, tensor_gran;
+  bool low_fp4, pv_bf16, v_convert, tensor_gran, pp;  // pp: ping-pong kernel (permuted, padded K operand)
   // byte offsets
   size_t q_hi, q_lo, k_hi, k_lo, v_codes, v_bf16;  // large buffers
   size_t small_begin, sf_q_hi, sf_q_lo, sf_k_hi, sf_k_lo, sf_v, qs_q, qs_k, ticket, small_end;
@@ -84,6 +94,8 @@ static Layout plan_layout(const DmaAttnArgs* a) {
   L.pv_bf16 = a->pv_mode == DMA_PV_BF16;
   L.v_convert = L.pv_bf16 && a->in_dtype != DMA_DT_BF16;
   L.tensor_gran = a->granularity == DMA_GRAN_TENSOR;
+  L.pp = !L.pv_bf16 && !force_single_stream();
+  const int64_t k_rows = L.pp ? L.lk_pad : a->len_k;
   const int64_t D = a->head_dim, DV = a->v_dim;
   L.ch_hi = (D / 32 + 3) / 4;
   L.ch_lo = a->low_format == DMA_FMT_NVFP4 ? (D / 16 + 3) / 4 : (D / 32 + 3) / 4;
@@ -95,8 +107,8 @@ static Layout plan_layout(const DmaAttnArgs* a) {
   };
   L.q_hi = take(L.mq * a->len_q * D);
   L.q_lo = L.low_fp4 ? take(L.mq * a->len_q * D / 2) : 0;
-  L.k_hi = take(L.mk * a->len_k * D);
-  L.k_lo = L.low_fp4 ? take(L.mk * a->len_k * D / 2) : 0;
+  L.k_hi = take(L.mk * k_rows * D);
+  L.k_lo = L.low_fp4 ? take(L.mk * k_rows * D / 2) : 0;
   L.v_codes = L.pv_bf16 ? 0 : take(L.mk * L.lk_pad * DV);
   L.v_bf16 = L.v_convert ? take(L.mk * a->len_k * DV * 2) : 0;
   L.small_begin = off;
@@ -190,7 +202,7 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
     uint8_t* sfh = ws + (isq ? L.sf_q_hi : L.sf_k_hi);
     float* qs = reinterpret_cast<float*>(ws + (isq ? L.qs_q : L.qs_k));
     if (q.rows == 0) continue;
-    if (int rc = quantize_impl(&q, sfl, sfh, qs, isq ? L.lq_pad : L.lk_pad, st)) return rc;
+    if (int rc = quantize_impl(&q, sfl, sfh, qs, isq ? L.lq_pad : L.lk_pad, st, (!isq && L.pp) ? 1 : 0)) return rc;
     g_launches += L.tensor_gran ? 2 : 1;
   }
   (void)nv;
@@ -222,16 +234,6 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
     }
   }
   return 0;
-}
-
-// DMA_SINGLE_STREAM=1 selects the one-stream kernel for the MXFP8 PV path too (A/B comparisons)
-static bool force_single_stream() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DMA_SINGLE_STREAM");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
 }
 
 static int num_sms() {
@@ -285,10 +287,11 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
   std::memset(&p, 0, sizeof(p));
   const int64_t lq_rows = a->len_q > 0 ? a->len_q : 1, lk_rows = a->len_k > 0 ? a->len_k : 1;
   if (int rc = make_map(&p.tm_q_hi, ws + L.q_hi, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, lq_rows, L.mq, (int)D)) return rc;
-  if (int rc = make_map(&p.tm_k_hi, ws + L.k_hi, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, lk_rows, L.mk, (int)D)) return rc;
+  const int64_t k_rows = L.pp ? L.lk_pad : lk_rows;
+  if (int rc = make_map(&p.tm_k_hi, ws + L.k_hi, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, k_rows, L.mk, (int)D)) return rc;
   if (L.low_fp4) {
     if (int rc = make_map(&p.tm_q_lo, ws + L.q_lo, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D / 2, lq_rows, L.mq, (int)D / 2)) return rc;
-    if (int rc = make_map(&p.tm_k_lo, ws + L.k_lo, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D / 2, lk_rows, L.mk, (int)D / 2)) return rc;
+    if (int rc = make_map(&p.tm_k_lo, ws + L.k_lo, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D / 2, k_rows, L.mk, (int)D / 2)) return rc;
   }
   if (L.pv_bf16) {
     const void* vsrc = L.v_convert ? static_cast<const void*>(ws + L.v_bf16) : a->v;
@@ -326,7 +329,7 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
   p.n_bh = static_cast<int>(L.mq);
   p.n_items = static_cast<int>(items);
   const int low = a->low_format == DMA_FMT_NVFP4 ? kLowNV : (a->low_format == DMA_FMT_MXFP4 ? kLowMX4 : kLowHigh);
-  if (!L.pv_bf16 && !force_single_stream()) {
+  if (L.pp) {
     // ping-pong kernel (block-scaled MXFP8 PV): pairs of heads share one query-tile plan
     PPParams q{};
     q.pairs_per_qt = static_cast<int>((L.mq + 1) / 2);
@@ -389,5 +392,15 @@ int dma_attention_fwd(const DmaAttnArgs* a, void* stream) {
 }
 
 int dma_last_launch_count(void) { return g_launches; }
+
+#ifdef DMA_PROFILE
+// profiling builds only: copy out and clear the softmax phase timers
+int dma_prof_read(unsigned long long* out, int n) {
+  DMA_CUDA_TRY(cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * (n < 32 ? n : 32)));
+  unsigned long long z[32] = {0};
+  DMA_CUDA_TRY(cudaMemcpyToSymbol(g_prof, z, sizeof(z)));
+  return 0;
+}
+#endif
 
 }  // extern "C"

@@ -73,7 +73,7 @@ static void launch_absmax(const DmaQuantArgs* a, unsigned long long* tmax, cudaS
 // Validates and runs quantize_dual with explicit operand-layout outputs (used by
 // the attention path as well as the public entry point).
 int quantize_impl(const DmaQuantArgs* a, uint8_t* sf_low_op, uint8_t* sf_high_op, float* qs_f32,
-                  int64_t rows_pad, cudaStream_t st) {
+                  int64_t rows_pad, cudaStream_t st, int key_perm) {
   DMA_CHECK_ARG(a && a->x, "quantize_dual: null input");
   DMA_CHECK_ARG(a->cols > 0 && a->cols % 32 == 0 && a->cols <= 1024,
                 "quantize_dual: cols must be a multiple of 32 in [32, 1024], got %lld", (long long)a->cols);
@@ -108,6 +108,12 @@ int quantize_impl(const DmaQuantArgs* a, uint8_t* sf_low_op, uint8_t* sf_high_op
   out.sf_high_op = sf_high_op;
   out.qs_f32 = qs_f32;
   out.rows_pad = rows_pad > 0 ? rows_pad : ((a->rows + 127) / 128) * 128;
+  out.key_perm = key_perm;
+  if (key_perm) {
+    const int64_t tpr = a->cols / 16;
+    DMA_CHECK_ARG(tpr <= 32 && (tpr & (tpr - 1)) == 0 && a->row_stride % 8 == 0 && a->mat_stride % 8 == 0,
+                  "quantize_dual: permuted operand layout needs cols in {32..512} (power of two) and aligned rows");
+  }
   if (a->x_dtype == DMA_DT_F64) dispatch_fmt<double>(a, tmax, out, st);
   else if (a->x_dtype == DMA_DT_F32) dispatch_fmt<float>(a, tmax, out, st);
   else dispatch_fmt<__nv_bfloat16>(a, tmax, out, st);
@@ -195,7 +201,7 @@ size_t dma_quantize_workspace_bytes(const DmaQuantArgs* a) {
 }
 
 int dma_quantize_dual(const DmaQuantArgs* a, void* stream) {
-  return quantize_impl(a, nullptr, nullptr, nullptr, 0, static_cast<cudaStream_t>(stream));
+  return quantize_impl(a, nullptr, nullptr, nullptr, 0, static_cast<cudaStream_t>(stream), 0);
 }
 
 int dma_dequantize(int32_t which, int32_t low_format, int32_t high_format, int32_t granularity, int64_t n_mat,

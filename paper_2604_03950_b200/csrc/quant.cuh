@@ -106,7 +106,17 @@ struct QuantOut {
   float* qs_f32;         // [mat, rows_pad] per-row S_q as f32 (TOKEN / TENSOR)
   uint32_t* nonfinite;
   int64_t rows_pad;      // rows rounded up to 128
+  int key_perm;          // operand rows permuted inside 128-row tiles (attn_pp.cuh), codes padded to rows_pad
 };
+
+// Key permutation of the ping-pong kernel (attn_pp.cuh): inside a 128-key tile,
+// key k = 32 G + 8 m + r sits in operand row 8 (4 G + r / 2) + 2 m + r % 2, and its
+// S_q^K in slot 32 m + 8 G + r.  (With this order the 16x256b TMEM fragment a
+// softmax thread holds covers exactly the keys whose P bytes it stores.)
+__host__ __device__ __forceinline__ int perm_row(int k) {
+  return 8 * (4 * (k >> 5) + ((k & 7) >> 1)) + 2 * ((k >> 3) & 3) + (k & 1);
+}
+__host__ __device__ __forceinline__ int perm_slot(int k) { return 32 * ((k >> 3) & 3) + 8 * (k >> 5) + (k & 7); }
 
 // 32-row x 4-SF interleave of one 128-row scale-factor atom (cutlass
 // Sm1xxBlockScaledBasicChunk: offset (r%32)*16 + (r/32)*4 + k)
@@ -447,11 +457,14 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
   if (!live) return;
 
   const int64_t rbase = mat * rows + row;
+  // operand row of the codes / scale-factor atoms (permuted inside 128-row tiles for attn_pp)
+  const int64_t orow = out.key_perm ? ((row & ~int64_t(127)) | perm_row(static_cast<int>(row & 127))) : row;
+  const int64_t cbase = out.key_perm ? mat * out.rows_pad + orow : rbase;
   const int col0 = part * 16;
   if (out.packed_low)
-    *reinterpret_cast<uint2*>(out.packed_low + rbase * (cols / 2) + col0 / 2) = make_uint2(packed[0], packed[1]);
+    *reinterpret_cast<uint2*>(out.packed_low + cbase * (cols / 2) + col0 / 2) = make_uint2(packed[0], packed[1]);
   if (out.high_codes)
-    *reinterpret_cast<uint4*>(out.high_codes + rbase * cols + col0) = make_uint4(codes[0], codes[1], codes[2], codes[3]);
+    *reinterpret_cast<uint4*>(out.high_codes + cbase * cols + col0) = make_uint4(codes[0], codes[1], codes[2], codes[3]);
   const int nsf_low = cols / (NV ? 16 : 32);
   const int chunks_low = (nsf_low + 3) >> 2;
   const int chunks_high = ((cols / 32) + 3) >> 2;
@@ -460,18 +473,21 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
   if (NV || even) {
     const int kb_low = NV ? part : (part >> 1);
     if (out.scales_low) out.scales_low[rbase * nsf_low + kb_low] = static_cast<uint8_t>(sc_low);
-    if (out.sf_low_op) out.sf_low_op[sf_atom_offset(mat, row, kb_low, rtiles, chunks_low)] = static_cast<uint8_t>(sc_low);
+    if (out.sf_low_op) out.sf_low_op[sf_atom_offset(mat, orow, kb_low, rtiles, chunks_low)] = static_cast<uint8_t>(sc_low);
   }
   if (even) {
     const int kb = part >> 1;
     if (out.scales_high) out.scales_high[rbase * (cols / 32) + kb] = static_cast<uint8_t>(sc_high);
-    if (out.sf_high_op) out.sf_high_op[sf_atom_offset(mat, row, kb, rtiles, chunks_high)] = static_cast<uint8_t>(sc_high);
+    if (out.sf_high_op) out.sf_high_op[sf_atom_offset(mat, orow, kb, rtiles, chunks_high)] = static_cast<uint8_t>(sc_high);
     if (GRAN == DMA_GRAN_BLOCK && out.quant_scale) out.quant_scale[rbase * (cols / 32) + kb] = sq;
   }
   if (part == 0) {
     if (GRAN == DMA_GRAN_TOKEN && out.quant_scale) out.quant_scale[rbase] = sq;
     if (GRAN == DMA_GRAN_TENSOR && out.quant_scale && row == 0) out.quant_scale[mat] = sq;
-    if (GRAN != DMA_GRAN_BLOCK && out.qs_f32) out.qs_f32[mat * out.rows_pad + row] = static_cast<float>(sq);
+    if (GRAN != DMA_GRAN_BLOCK && out.qs_f32) {
+      const int64_t slot = out.key_perm ? ((row & ~int64_t(127)) | perm_slot(static_cast<int>(row & 127))) : row;
+      out.qs_f32[mat * out.rows_pad + slot] = static_cast<float>(sq);
+    }
   }
 }
 
