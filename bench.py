@@ -250,11 +250,19 @@ def main():
         dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
         e2e_steps = max(3, min(args.steps, 5))
 
+        shard = None
+        if world > 1:
+            # global problem = one batch element per rank; O is reassembled on every rank
+            from paper_2604_03950_b200.sharding import gather, plan_shard
+            shard = plan_shard(world * B, H, KVH, world, rank)
+
         def e2e_step():
             dq.copy_(hq, non_blocking=True)
             dk.copy_(hk, non_blocking=True)
             dv.copy_(hv, non_blocking=True)
             fwd(dq, dk, dv, out=out)
+            if shard is not None:
+                gather(out.reshape(1, B * H, N, d), shard, world * B, H)  # NCCL all_gather of O
             ho.copy_(out, non_blocking=True)
 
         e2e_step()
@@ -274,7 +282,9 @@ def main():
         d2h = out.numel() * out.element_size()
         e2e = {"value": world * F / (float(te.item()) * 1e-3) / 1e12, "unit": "TFLOPS",
                "ms_per_step": float(te.item()), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "api": "paper_2604_03950_b200.DmaAttention.__call__ (pinned host buffers)"}
+               "api": "paper_2604_03950_b200.DmaAttention.__call__ (pinned host buffers)"
+                      + (" + sharding.gather (NCCL all_gather of O)" if world > 1 else ""),
+               "gather_bytes_per_step": (world * d2h if world > 1 else 0)}
 
     if rank == 0:
         peaks, src = load_peaks()
