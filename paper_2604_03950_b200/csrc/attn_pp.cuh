@@ -90,8 +90,9 @@ struct PPCfg {
   static constexpr int oSfQ = oV + kNV * kVBytes;             // [2 slot][2 stream][kSfQ]
   static constexpr int oSfK = oSfQ + 4 * kSfQ;                // [kNK][kChK][512]
   static constexpr int oSfV = oSfK + kNK * kChK * 512;        // [kNV][512]
-  static constexpr int oSqK = oSfV + kNV * 512;               // [2 stream][kNS][512]
-  static constexpr int oSfP = oSqK + 2 * kNS * 512;           // 512
+  static constexpr int kSqkBytes = 4 * kSqkTile;              // 576: S_q^K of one tile, bank-padded
+  static constexpr int oSqK = oSfV + kNV * 512;               // [2 stream][kNS][kSqkBytes]
+  static constexpr int oSfP = oSqK + 2 * kNS * kSqkBytes;     // 512
   static constexpr int oSch = oSfP + 512;                     // [kNSch] int
   static constexpr int oBar = oSch + 64;
   static constexpr int kSmemBytes = oBar + 512 + 1024;
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
               const int sl = sc[y] % C::kNS;
               ptx::mbar_wait(sq_empty + y * C::kNS + sl, ((sc[y] / C::kNS) & 1) ^ 1);
             }
-            ptx::mbar_arrive_expect_tx(k_full + ks, kbytes + 512 * ch + 512 * (s1 - s0));
+            ptx::mbar_arrive_expect_tx(k_full + ks, kbytes + 512 * ch + C::kSqkBytes * (s1 - s0));
             ptx::tma_load_3d(smem + C::oK + ks * C::kKBytes, hi ? &p.tm_k_hi : &p.tm_k_lo, k_full + ks, 0,
                              t * C::kBN, mk[x]);
             const uint8_t* sfsrc = (hi ? p.sf_k_hi : p.sf_k_lo) +
@@ -267,8 +268,8 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
             for (int y = s0; y < s1; ++y) {
               const int sl = sc[y] % C::kNS;
               ++sc[y];
-              ptx::bulk_load(smem + C::oSqK + (y * C::kNS + sl) * 512,
-                             p.qs_k + static_cast<int64_t>(mk[x]) * p.lk_pad + t * C::kBN, 512, k_full + ks);
+              ptx::bulk_load(smem + C::oSqK + (y * C::kNS + sl) * C::kSqkBytes,
+                             p.qs_k + (static_cast<int64_t>(mk[x]) * rt_k + t) * kSqkTile, C::kSqkBytes, k_full + ks);
             }
           }
           for (int x = 0; x < nk; ++x) {
@@ -502,8 +503,8 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
           const int sl = sc % C::kNS;
           ++sc;
           if (two_level) {
-            // this thread's 32 factors are contiguous: [32 m + 2 g + b]
-            const uint32_t sqk = ptx::smem_u32(smem + C::oSqK + (x * C::kNS + sl) * 512) + 128 * m4;
+            // this thread's 32 factors are contiguous: [36 m + 2 g + b]
+            const uint32_t sqk = ptx::smem_u32(smem + C::oSqK + (x * C::kNS + sl) * C::kSqkBytes) + 144 * m4;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {  // factors for columns g = 2j, 2j + 1
               const float4 f = ptx::lds_f4(sqk + 16 * j);

@@ -118,7 +118,7 @@ static Layout plan_layout(const DmaAttnArgs* a) {
   L.sf_k_lo = L.low_fp4 ? take(L.mk * (L.lk_pad / 128) * L.ch_lo * 512) : 0;
   L.sf_v = L.pv_bf16 ? 0 : take(L.mk * (L.lk_pad / 128) * ((DV + 127) / 128) * 512);
   L.qs_q = take(L.mq * L.lq_pad * 4);
-  L.qs_k = take(L.mk * L.lk_pad * 4);
+  L.qs_k = take(L.pp ? L.mk * (L.lk_pad / 128) * kSqkTile * 4 : L.mk * L.lk_pad * 4);
   L.ticket = take(64);  // dynamic pair scheduler ticket (zeroed with the small region; self-resetting)
   L.small_end = off;
   L.absmax_q = L.tensor_gran ? take(L.mq * 8) : 0;

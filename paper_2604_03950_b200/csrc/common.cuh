@@ -103,4 +103,16 @@ struct Plan {
   }
 };
 
+// Key permutation of the ping-pong kernel (attn_pp.cuh): inside a 128-key tile,
+// key k = 32 G + 8 m + r sits in operand row 8 (4 G + r / 2) + 2 m + r % 2, and its
+// S_q^K in slot 36 m + 8 G + r of the tile's 144 (kSqkTile) slots.  (With this order the 16x256b TMEM fragment a
+// softmax thread holds covers exactly the keys whose P bytes it stores.)
+__host__ __device__ __forceinline__ int perm_row(int k) {
+  return 8 * (4 * (k >> 5) + ((k & 7) >> 1)) + 2 * ((k >> 3) & 3) + (k & 1);
+}
+// S_q^K slots per 128-key tile: 4 groups of 32 (one per m), padded to 36 so the
+// four groups start in different shared-memory banks
+constexpr int kSqkTile = 144;
+__host__ __device__ __forceinline__ int perm_slot(int k) { return 36 * ((k >> 3) & 3) + 8 * (k >> 5) + (k & 7); }
+
 }  // namespace dma

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
+#include "common.cuh"
 #include "ptx.cuh"
 
 namespace dma {
@@ -109,14 +110,6 @@ struct QuantOut {
   int key_perm;          // operand rows permuted inside 128-row tiles (attn_pp.cuh), codes padded to rows_pad
 };
 
-// Key permutation of the ping-pong kernel (attn_pp.cuh): inside a 128-key tile,
-// key k = 32 G + 8 m + r sits in operand row 8 (4 G + r / 2) + 2 m + r % 2, and its
-// S_q^K in slot 32 m + 8 G + r.  (With this order the 16x256b TMEM fragment a
-// softmax thread holds covers exactly the keys whose P bytes it stores.)
-__host__ __device__ __forceinline__ int perm_row(int k) {
-  return 8 * (4 * (k >> 5) + ((k & 7) >> 1)) + 2 * ((k >> 3) & 3) + (k & 1);
-}
-__host__ __device__ __forceinline__ int perm_slot(int k) { return 32 * ((k >> 3) & 3) + 8 * (k >> 5) + (k & 7); }
 
 // 32-row x 4-SF interleave of one 128-row scale-factor atom (cutlass
 // Sm1xxBlockScaledBasicChunk: offset (r%32)*16 + (r/32)*4 + k)
@@ -485,8 +478,11 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
     if (GRAN == DMA_GRAN_TOKEN && out.quant_scale) out.quant_scale[rbase] = sq;
     if (GRAN == DMA_GRAN_TENSOR && out.quant_scale && row == 0) out.quant_scale[mat] = sq;
     if (GRAN != DMA_GRAN_BLOCK && out.qs_f32) {
-      const int64_t slot = out.key_perm ? ((row & ~int64_t(127)) | perm_slot(static_cast<int>(row & 127))) : row;
-      out.qs_f32[mat * out.rows_pad + slot] = static_cast<float>(sq);
+      if (out.key_perm)
+        out.qs_f32[(mat * (out.rows_pad >> 7) + (row >> 7)) * kSqkTile + perm_slot(static_cast<int>(row & 127))] =
+            static_cast<float>(sq);
+      else
+        out.qs_f32[mat * out.rows_pad + row] = static_cast<float>(sq);
     }
   }
 }
