@@ -322,7 +322,7 @@ def main():
                        "parallelism": f"batch x head sharding, {world} rank(s), no hot-path collective",
                        "l2": "inputs (805 MB bf16 Q/K/V at c3) exceed the 126 MB L2; no flush"},
             "phases_ms": {"quantize": quant_ms, "attention": core_ms},
-            "roofline": {"bound": "tensor", "kernel": "dma_attn_kernel", "achieved": achieved,
+            "roofline": {"bound": "tensor", "kernel": "dma_attn_pp_kernel" if args.pv == "mxfp8" else "dma_attn_kernel", "achieved": achieved,
                          "peak": peak_mix, "unit": "TFLOP/s", "frac": achieved / peak_mix,
                          "traffic": traffic,
                          "peak_source": f"{src} bf16 {bf16:.0f} TF/s x (fp4 4x, fp8 2x) mix-weighted by Bit_high",

@@ -14,6 +14,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:dma_attn -s 3 -c 1 -o gpurun_out/attn_full -f \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; tail -3 gpurun_out/ncu_full.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:quant_rows -s 6 -c 1 -o gpurun_out/quant_full -f \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:quant16 -s 6 -c 1 -o gpurun_out/quant_full -f \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_quant.log 2>&1; tail -3 gpurun_out/ncu_quant.log
 fi
