@@ -343,5 +343,73 @@ __device__ __forceinline__ uint8_t cvt_e2m1x2(float lo, float hi) {
   return static_cast<uint8_t>(r);
 }
 
+
+// ---------------------------------------------------------------- warp-uniform issue
+// Versions of the single-thread async ops for code that a whole warp executes in
+// lock-step (warp-uniform control flow): elect.sync picks one lane inside the asm,
+// so ptxas emits ONE warp-level UTC*/UTMA*/SYNCS instruction with its operands in
+// uniform registers -- no per-thread ELECT/BRA.U.ANY loop and no R2UR moves, which
+// made a lane-0-only issuer latency-bound (~15 instructions per tcgen05 op).
+namespace wu {
+#define DMA_WU_ELECT "elect.sync _|e, 0xffffffff;\n\t"
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .pred e;\n\t" DMA_WU_ELECT "@e mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n\t}"
+               ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .pred e;\n\t" DMA_WU_ELECT
+               "@e mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n\t}"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile("{\n\t.reg .pred e;\n\t" DMA_WU_ELECT
+               "@e cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%3, %4, %5}], [%2];\n\t}"
+               ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("{\n\t.reg .pred e;\n\t" DMA_WU_ELECT
+               "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}"
+               ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("{\n\t.reg .pred e;\n\t" DMA_WU_ELECT
+               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+               ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_cp_sf(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("{\n\t.reg .pred e;\n\t" DMA_WU_ELECT "@e tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;\n\t}"
+               ::"r"(taddr), "l"(sdesc) : "memory");
+}
+#define DMA_WU_MMA(name, kind_str, a_operand, a_constraint, a_type)                                          \
+  __device__ __forceinline__ void name(uint32_t d, a_type a, uint64_t bdesc, uint32_t idesc, uint32_t sfa,    \
+                                       uint32_t sfb, uint32_t acc) {                                         \
+    asm volatile("{\n\t.reg .pred p, e;\n\t setp.ne.b32 p, %6, 0;\n\t" DMA_WU_ELECT                           \
+                 "@e tcgen05.mma.cta_group::1." kind_str " [%0], " a_operand ", %2, %3, [%4], [%5], p;\n\t}"    \
+                 ::"r"(d), a_constraint(a), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(acc)               \
+                 : "memory");                                                                                \
+  }
+DMA_WU_MMA(mma_mxf8f6f4, "kind::mxf8f6f4.block_scale.scale_vec::1X", "%1", "l", uint64_t)
+DMA_WU_MMA(mma_mxf8f6f4_ts, "kind::mxf8f6f4.block_scale.scale_vec::1X", "[%1]", "r", uint32_t)
+DMA_WU_MMA(mma_nvf4, "kind::mxf4nvf4.block_scale.scale_vec::4X", "%1", "l", uint64_t)
+DMA_WU_MMA(mma_mxf4, "kind::mxf4.block_scale.scale_vec::2X", "%1", "l", uint64_t)
+#undef DMA_WU_MMA
+}  // namespace wu
+
+// Low word of a UMMA smem descriptor for a 16-B aligned shared address below 256 KB:
+// the start-address field is addr >> 4 (14 bits, never overflows) and the LBO field
+// sits above it, so the masks of smem_desc reduce to an add.
+__host__ __device__ __forceinline__ uint32_t desc_lo(uint32_t saddr, uint32_t lbo_bytes) {
+  return (saddr >> 4) + ((lbo_bytes >> 4) << 16);
+}
+__host__ __device__ __forceinline__ uint32_t desc_hi(uint32_t sbo_bytes, uint32_t layout) {
+  return (sbo_bytes >> 4) | (1u << 14) | ((layout & 7) << 29);
+}
+__host__ __device__ __forceinline__ uint64_t desc_of(uint32_t lo, uint32_t hi) {
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
 }  // namespace ptx
 }  // namespace dma

@@ -39,3 +39,11 @@ tot = sum(buf[:10])
 print(f"{cfgn}: kernel {e0.elapsed_time(e1):.3f} ms; softmax-warp cycles by phase:")
 for i, n in enumerate(names):
     print(f"  {n:18s} {buf[i] / tot * 100:6.1f}%")
+for title, base, nm in (("MMA issuer", 10, ["issue/other", "wait sched", "wait Q", "wait S free", "wait K", "wait P",
+                                           "wait V", "SF copy", "MMA issue", "commit"]),
+                        ("producer", 22, ["issue/other", "wait sched slot", "wait Q slot", "wait K slot",
+                                          "wait SqK slot", "wait V slot"])):
+    tot = sum(buf[base:base + len(nm)]) or 1
+    print(f"{title} cycles by phase:")
+    for i, n in enumerate(nm):
+        print(f"  {n:18s} {buf[base + i] / tot * 100:6.1f}%")
