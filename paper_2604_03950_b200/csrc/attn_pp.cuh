@@ -57,16 +57,44 @@ __device__ unsigned long long g_prof[32];
 #define PROF_FLUSH(base, n) do {} while (0)
 #endif
 
+// Optional event trace of CTA 0 (-DDMA_TRACE): clock64 << 8 | event per role
+// (0/1 softmax stream A/B, 2 MMA issuer, 3 producer), read back with dma_trace_read.
+#ifdef DMA_TRACE
+__device__ unsigned long long g_trace[4][4096];
+__device__ unsigned int g_trace_n[4];
+// the event index lives in a register (trace_i, declared by TRACE_DECL in each role);
+// stores are fire-and-forget, so a trace point costs a few issue slots
+#define TRACE_DECL unsigned int trace_i = 0;
+#define TRACE(cond, role, ev)                                                                 \
+  do {                                                                                        \
+    if ((cond) && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && trace_i < 4096) {             \
+      g_trace[role][trace_i] = (static_cast<unsigned long long>(clock64()) << 8) | (ev);      \
+      g_trace_n[role] = ++trace_i;                                                            \
+    }                                                                                         \
+  } while (0)
+#else
+#define TRACE_DECL
+#define TRACE(cond, role, ev) do {} while (0)
+#endif
+
+#ifndef DMA_PP_POLY
+#define DMA_PP_POLY 0
+#endif
+// pairs (out of every 4) of the softmax exponentials computed by the degree-4 FMA-pipe
+// polynomial (exp2_poly2) instead of MUFU.EX2
+constexpr int kPolyPP = DMA_PP_POLY;
+
 #ifndef DMA_PP_TURNS
 #define DMA_PP_TURNS 0
 #endif
 // 1: the two softmax warpgroups take strict turns for their exp2 phases
 constexpr bool kTurns = DMA_PP_TURNS != 0;
-#ifndef DMA_PP_FRAG16
-#define DMA_PP_FRAG16 0
+#ifndef DMA_PP_SPLIT
+#define DMA_PP_SPLIT 1
 #endif
-// 1: softmax threads hold 4 rows x 32 columns (16x256b TMEM shape); 0: one row each (32x32b)
-constexpr bool kFrag16 = DMA_PP_FRAG16 != 0;
+// softmax warpgroups per stream: 1 = a thread owns a whole S row (128 columns);
+// 2 = two warps share each row, one key half each (4 softmax warps per SM sub-partition)
+constexpr int kSplit = DMA_PP_SPLIT;
 
 struct PPParams {
   int n_pairs;
@@ -78,7 +106,15 @@ struct PPParams {
 template <int D, int DV, int LOW>
 struct PPCfg {
   static constexpr int kBM = 128, kBN = 128;
-  static constexpr int kNK = 4, kNV = 3, kNS = 4, kNSch = 4;
+  static constexpr int kNK = kSplit == 2 ? 3 : 4, kNV = 3, kNS = 4, kNSch = 4;
+  static constexpr int kSoftWarps = 8 * kSplit;        // softmax warps (2 streams x kSplit warpgroups)
+  static constexpr int kThreads = 32 * (kSoftWarps + 4);  // + producer, MMA issuer, 2 idle
+  // setmaxnreg budgets: softmax warpgroups grow, the producer/MMA warpgroup shrinks.  The
+  // CTA's register pool is what the launch allocated (kThreads x the launch-bound count,
+  // 168 / 96), so 2 x 128 x 216 + 128 x 72 <= 384 x 168 and 4 x 128 x 104 + 128 x 64 <= 640 x 96.
+  static constexpr int kRegSoft = kSplit == 1 ? 216 : 104;
+  static constexpr int kRegCtl = kSplit == 1 ? 72 : 64;
+  static_assert(kSoftWarps * 32 * kRegSoft + 128 * kRegCtl <= kThreads * (kSplit == 1 ? 168 : 96), "register pool");
   static constexpr int kQHiBytes = kBM * D;
   static constexpr int kQLoBytes = kBM * D / 2;
   static constexpr int kQStream = ((kQHiBytes + (LOW != kLowHigh ? kQLoBytes : 0) + 1023) / 1024) * 1024;
@@ -99,7 +135,8 @@ struct PPCfg {
   static constexpr int oSqK = oSfV + kNV * 512;               // [2 stream][kNS][kSqkBytes]
   static constexpr int oSfP = oSqK + 2 * kNS * kSqkBytes;     // 512
   static constexpr int oSch = oSfP + 512;                     // [kNSch] int
-  static constexpr int oBar = oSch + 64;
+  static constexpr int oRed = oSch + 64;                      // [2 parity][2 stream][2 half][128] f32 row maxima, then l
+  static constexpr int oBar = oRed + (kSplit == 2 ? 2 * 4096 : 0);
   static constexpr int kSmemBytes = oBar + 512 + 1024;
   // TMEM columns
   static constexpr uint32_t tS = 0, tSfP = 496;
@@ -131,6 +168,18 @@ __device__ __forceinline__ int mat_k_of(const AttnParams& p, int bh) {
 }
 
 
+// exp2 / E4M3 pack as volatile asm: the softmax orders them explicitly (software pipelining)
+__device__ __forceinline__ float exp2_ordered(float x) {
+  float y;
+  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t cvt_e4m3x2_ordered(float lo, float hi) {
+  uint16_t r;
+  asm volatile("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 // one 32-column chunk c of an output row: O[row, 32c + i] = acc[i] * inv_l (bf16 or f32)
 template <int DV>
 __device__ __forceinline__ void store_orow(const AttnParams& p, int64_t orow, int c, const uint32_t (&rr)[32],
@@ -158,7 +207,7 @@ __device__ __forceinline__ void store_orow(const AttnParams& p, int64_t orow, in
 }
 
 template <int D, int DV, int LOW>
-__global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_constant__ AttnParams p,
+__global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_kernel(const __grid_constant__ AttnParams p,
                                                              const __grid_constant__ PPParams pp) {
   using C = PPCfg<D, DV, LOW>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -183,14 +232,14 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rt_q = p.lq_pad >> 7, rt_k = p.lk_pad >> 7;
 
-  constexpr int kProducer = 8, kMma = 9;  // warps 0-7: softmax (stream = warp / 4)
+  constexpr int kProducer = C::kSoftWarps, kMma = C::kSoftWarps + 1;  // warps below: softmax
   if (warp == kProducer) {
     if (lane == 0) {
       for (int i = 0; i < 2; ++i) {
         ptx::mbar_init(q_full + i, 1);
         ptx::mbar_init(q_empty + i, 1);
         ptx::mbar_init(s_full + i, 1);
-        ptx::mbar_init(p_full + i, 4);
+        ptx::mbar_init(p_full + i, 4 * kSplit);
         ptx::mbar_init(o_done + i, 1);
       }
       for (int i = 0; i < C::kNK; ++i) {
@@ -201,11 +250,11 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
         ptx::mbar_init(v_full + i, 1);
         ptx::mbar_init(v_empty + i, 1);
       }
-      for (int i = 0; i < 2 * C::kNS; ++i) ptx::mbar_init(sq_empty + i, 4);
-      ptx::mbar_init(s_free, 4);
+      for (int i = 0; i < 2 * C::kNS; ++i) ptx::mbar_init(sq_empty + i, 4 * kSplit);
+      ptx::mbar_init(s_free, 4 * kSplit);
       for (int i = 0; i < C::kNSch; ++i) {
         ptx::mbar_init(sch_full + i, 1);
-        ptx::mbar_init(sch_empty + i, 1 + 8);
+        ptx::mbar_init(sch_empty + i, 1 + C::kSoftWarps);
       }
       ptx::fence_barrier_init();
       ptx::tma_prefetch_desc(&p.tm_q_hi);
@@ -229,9 +278,9 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp >= 8) {
-  // register budget: warpgroup 2 gives registers to the softmax warpgroups
-  ptx::setmaxnreg_dec<72>();
+  if (warp >= C::kSoftWarps) {
+  // register budget: the last warpgroup gives registers to the softmax warpgroups
+  ptx::setmaxnreg_dec<C::kRegCtl>();
   // Producer and MMA issuer run as whole warps in lock-step (warp-uniform control
   // flow) and issue their async ops through ptx::wu: one elected lane, operands in
   // uniform registers, one SASS instruction per TMA / tcgen05 op.
@@ -348,6 +397,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
     ptx::wu::tc_cp_sf(tmem + C::tSfP, sf_desc(C::oSfP));
     PROF_DECL
     uint32_t ks = 0, kph = 0, vs = 0, vph = 0, su = 0, po = 0, pvc[2] = {0, 0};
+    TRACE_DECL
     // instruction descriptors (loop-invariant)
     const uint32_t hf = static_cast<uint32_t>(p.hfmt);
     for (uint32_t i = 0;; ++i) {
@@ -380,9 +430,11 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
         plan.entry(e, t, hi);
         if (LOW == kLowHigh) hi = true;
         // the single S buffer: wait until its previous user copied it out
+        TRACE(true, 2, 26 + x);
         PROF_MARK(0);
         ptx::mbar_wait(s_free, (su & 1) ^ 1);
         PROF_MARK(3);
+        TRACE(true, 2, 10 + x);
         ++su;
         ptx::tc_fence_after();
         const uint32_t oq = C::oQ + (qs * 2 + x) * C::kQStream;
@@ -398,6 +450,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
           PROF_MARK(0);
           ptx::mbar_wait(k_full + ks, kph);
           PROF_MARK(4);
+          TRACE(true, 2, 18 + x);
           if (++ks == C::kNK) { ks = 0; kph ^= 1; }
           ptx::tc_fence_after();
         } else {
@@ -406,9 +459,12 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
         const uint32_t kslt = kslot[x];
         const int ch = hi ? C::kChHi : C::kChLo;
         PROF_MARK(0);
+#ifndef DMA_EXP_NOSFK
         for (int j = 0; j < ch; ++j)
           ptx::wu::tc_cp_sf(tmem + C::tSfK(x) + 4 * j, sf_desc(C::oSfK + kslt * 512 * C::kChK + 512 * j));
+#endif
         PROF_MARK(7);
+        TRACE(true, 2, 20 + x);
         const uint32_t kaddr = sbase + C::oK + kslt * C::kKBytes;
         const uint32_t tsfq = tmem + C::tSfQ(x), tsfk = tmem + C::tSfK(x), tSd = tmem + C::tS;
         if (hi) {
@@ -439,9 +495,11 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
           }
         }
         PROF_MARK(8);
+        TRACE(true, 2, 12 + x);
         if (x == ns - 1 || !shared_kv) ptx::wu::tc_commit(k_empty + kslt);  // last reader of this K slot
         ptx::wu::tc_commit(s_full + x);
         if (e == plan.n - 1 && x == ns - 1) ptx::wu::tc_commit(q_empty + qs);  // Q slot free after these
+        TRACE(true, 2, 28 + x);
         PROF_MARK(9);
       };
 
@@ -449,6 +507,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
         PROF_MARK(0);
         ptx::mbar_wait(p_full + x, pvc[x] & 1);
         PROF_MARK(5);
+        TRACE(true, 2, 14 + x);
         ++pvc[x];
         ptx::tc_fence_after();
         if (x == 0 || !shared_kv) {
@@ -456,6 +515,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
           PROF_MARK(0);
           ptx::mbar_wait(v_full + vs, vph);
           PROF_MARK(6);
+          TRACE(true, 2, 22 + x);
           if (++vs == C::kNV) { vs = 0; vph ^= 1; }
           ptx::tc_fence_after();
         } else {
@@ -476,8 +536,10 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
                                    tmem + C::tSfV(x), !(e == 0 && kk == 0));
         }
         PROF_MARK(8);
+        TRACE(true, 2, 16 + x);
         if (x == ns - 1 || !shared_kv) ptx::wu::tc_commit(v_empty + vslt);
         ptx::wu::tc_commit(o_done + x);
+        TRACE(true, 2, 24 + x);
         PROF_MARK(9);
       };
 
@@ -495,24 +557,39 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
     PROF_MARK(0);
     PROF_FLUSH(10, 10);
   }
-  } else if (!kFrag16) {
-    ptx::setmaxnreg_inc<216>();  // the 128-value S row stays in registers
-    // =========================== softmax (one warpgroup per stream) ===========================
+  } else {
+    ptx::setmaxnreg_inc<C::kRegSoft>();
+    // =========================== softmax (kSplit warpgroups per stream) ===========================
     // TMEM is read in the 32x32b shape: thread = one query row (lane of its warp's
-    // 32-lane sub-partition), all 128 S columns.  Row max / sum need no shuffles and
-    // the per-row bookkeeping (max, alpha, bias) is done once per thread.  K rows are
-    // permuted inside every 128-key tile (perm_row, for the 16x256b variant); since
-    // a thread owns the whole row, undoing it is register renaming at compile time:
+    // 32-lane sub-partition) and NK = 128 / kSplit S columns.  With kSplit = 2 the two
+    // warps sharing a row each take one half of the key tile (4 softmax warps per SM
+    // sub-partition, for latency hiding) and exchange their partial row maxima through
+    // shared memory.  K rows are permuted inside every 128-key tile (perm_row); the
+    // permutation maps 32-key group G onto S columns [32G, 32G + 32), so a thread's key
+    // half is its column half and undoing the order is compile-time register renaming:
     // key k sits in S column perm_row(k), its S_q^K in slot perm_slot(k).
-    const int x = warp >> 2;  // stream
+    constexpr int NK = 128 / kSplit;  // keys (S columns) per thread
+    constexpr int NW = NK / 4;        // E4M3 P words per thread
+    constexpr int NG = NK / 32;       // 32-key groups per thread
+    constexpr int OC = DV / kSplit;   // O columns per thread
+    const int x = warp / (4 * kSplit);  // stream
+    const int hh = kSplit == 1 ? 0 : (warp >> 2) & 1;
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
+    const int kb = NK * hh;  // first key / S column of this thread's half
     const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
-    // lazy rescaling (see the 16x256b variant below): P <= 2^kLazy, stored as E4M3(P * 2^(8 - kLazy))
+    const uint32_t xbar = 3 + x * 4 + quad;
+    const bool tw = quad == 0 && hh == 0;  // the traced warp of this stream (DMA_TRACE)
+    (void)tw;
+    TRACE_DECL  // named barrier of the kSplit warps sharing these rows
+    float* red = reinterpret_cast<float*>(smem + C::oRed);  // [2 parity][2 stream][2 half][128]
+    // lazy rescaling (the FA4 trick): a row keeps its running max until a tile raises it
+    // by more than kLazy (log2 units), so O is rarely rescaled; P <= 2^kLazy is stored as
+    // E4M3(P * 2^(8 - kLazy)) <= 256 < 448.
     constexpr float kLazy = 4.f;
     constexpr float kPShift = 8.f - kLazy;
     uint32_t g = 0, sc = 0;
-    if (kTurns && x == 1) ptx::named_bar_arrive(1, 256);  // A takes the first exp phase
+    if (kTurns && x == 1) ptx::named_bar_arrive(1, 256 * kSplit);  // A takes the first exp phase
     PROF_DECL
 
     for (uint32_t it = 0;; ++it) {
@@ -545,30 +622,33 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
         PROF_MARK(9);
         ptx::mbar_wait(s_full + x, g & 1);
         ptx::tc_fence_after();
+        TRACE(tw, x, 1);
         PROF_MARK(0);
-        // S columns [0, 64) hold keys [0, 64) (permuted), [64, 128) keys [64, 128):
-        // load the first half, start the second, scale the first while it lands
-        uint32_t sr[128];
-        ptx::tmem_ld32(tmem + C::tS + lane_base, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-        ptx::tmem_ld32(tmem + C::tS + lane_base + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+        // load the first half of this thread's columns, start the second, scale the first while it lands
+        uint32_t sr[NK];
+#pragma unroll
+        for (int c = 0; c < NK / 2; c += 32)
+          ptx::tmem_ld32(tmem + C::tS + lane_base + kb + c, *reinterpret_cast<uint32_t(*)[32]>(&sr[c]));
         ptx::tmem_ld_wait();
-        ptx::tmem_ld32(tmem + C::tS + lane_base + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
-        ptx::tmem_ld32(tmem + C::tS + lane_base + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
+#pragma unroll
+        for (int c = NK / 2; c < NK; c += 32)
+          ptx::tmem_ld32(tmem + C::tS + lane_base + kb + c, *reinterpret_cast<uint32_t(*)[32]>(&sr[c]));
         PROF_MARK(1);
-        // t[k] = S[key k] * S_q^K[k] in natural key order (FMUL2 over key pairs 4w + {0,1}, {2,3},
-        // which are adjacent S columns perm_row(4w) + {0, 1})
+        // tv[i] = S[key kb + i] * S_q^K[kb + i], natural key order (FMUL2 over key pairs
+        // 4w + {0,1}, {2,3}, which are adjacent S columns perm_row(4w) + {0, 1})
         const int sl = sc % C::kNS;
         ++sc;
-        const uint32_t sqk = ptx::smem_u32(smem + C::oSqK + (x * C::kNS + sl) * C::kSqkBytes);
-        float tv[128];
+        const uint32_t sqk = ptx::smem_u32(smem + C::oSqK + (x * C::kNS + sl) * C::kSqkBytes) + kb;
+        float tv[NK];
         auto scale_words = [&](int w0) {
 #pragma unroll
-          for (int w = w0; w < w0 + 16; ++w) {
+          for (int w = w0; w < w0 + NW / 2; ++w) {
+            // perm_row(kb + i) = kb + perm_row(i) for kb in {0, 64}: compile-time register indices
             const int c0 = perm_row(4 * w), c1 = perm_row(4 * w + 2);
             float2 a = make_float2(__uint_as_float(sr[c0]), __uint_as_float(sr[c0 + 1]));
             float2 b = make_float2(__uint_as_float(sr[c1]), __uint_as_float(sr[c1 + 1]));
             if (two_level) {
-              const float4 f = ptx::lds_f4(sqk + 4 * perm_slot(4 * w));
+              const float4 f = ptx::lds_f4(sqk + 4 * perm_slot(4 * w));  // perm_slot(kb + i) = perm_slot(i) + kb / 4
               a = __fmul2_rn(a, make_float2(f.x, f.y));
               b = __fmul2_rn(b, make_float2(f.z, f.w));
             }
@@ -583,7 +663,8 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(s_free);  // S buffer may be overwritten by the next QK
-        scale_words(16);
+        TRACE(tw, x, 2);
+        scale_words(NW / 2);
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(sq_empty + x * C::kNS + sl);
         PROF_MARK(2);
@@ -591,19 +672,27 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
         const int kvalid = p.lk - k0;
         const bool need_causal = p.causal && (k0 + (kvalid < C::kBN ? kvalid : C::kBN) - 1 > q0);
         if (need_causal || kvalid < C::kBN) {
-          const int lim = need_causal ? min(qrow - k0 + 1, kvalid) : kvalid;
+          const int lim = (need_causal ? min(qrow - k0 + 1, kvalid) : kvalid) - kb;
 #pragma unroll
-          for (int j = 0; j < 128; ++j)
+          for (int j = 0; j < NK; ++j)
             if (j >= lim) tv[j] = -INFINITY;
         }
-        float mx = ptx::fmax3(tv[0], tv[1], tv[2]);
-        float mx2 = ptx::fmax3(tv[3], tv[4], tv[5]);
+        // row max: 4 independent FMNMX3 chains
+        float m4[4] = {fmaxf(tv[0], tv[1]), fmaxf(tv[2], tv[3]), fmaxf(tv[4], tv[5]), fmaxf(tv[6], tv[7])};
 #pragma unroll
-        for (int j = 6; j < 126; j += 4) {
-          mx = ptx::fmax3(mx, tv[j], tv[j + 1]);
-          mx2 = ptx::fmax3(mx2, tv[j + 2], tv[j + 3]);
+        for (int j = 8; j < NK; j += 8) {
+          m4[0] = ptx::fmax3(m4[0], tv[j], tv[j + 1]);
+          m4[1] = ptx::fmax3(m4[1], tv[j + 2], tv[j + 3]);
+          m4[2] = ptx::fmax3(m4[2], tv[j + 4], tv[j + 5]);
+          m4[3] = ptx::fmax3(m4[3], tv[j + 6], tv[j + 7]);
         }
-        mx = ptx::fmax3(mx, mx2, fmaxf(tv[126], tv[127]));
+        float mx = fmaxf(ptx::fmax3(m4[0], m4[1], m4[2]), m4[3]);
+        if (kSplit == 2) {
+          float* rb = red + ((g & 1) * 2 + x) * 256;
+          rb[hh * 128 + row] = mx;
+          ptx::named_bar_sync(xbar, 64);
+          mx = fmaxf(mx, rb[(hh ^ 1) * 128 + row]);
+        }
         const float rowf = two_level ? sq_q : 1.0f;
         const float m_cand = fmaxf(m_run, mx * rowf);
         const bool upd = m_cand > m_run + kLazy;  // always for the first live tile (m_run = -inf)
@@ -612,6 +701,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
         const float alpha = (dead || !upd) ? 1.0f : fast_exp2(m_run - m_new);  // m_run = -inf -> 0
         const float bias = dead ? 0.f : (kPShift - m_new);
         m_run = m_new;
+        TRACE(tw, x, 3);
         PROF_MARK(3);
         // P_x (and O_x) are read by PV(e-1): wait for it before overwriting
         if (e > 0) {
@@ -619,41 +709,61 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
           ptx::tc_fence_after();
         }
         PROF_MARK(4);
-        // exp phases of the two streams alternate (A, B, A, B, ...): MUFU.EX2 is the
-        // shared bottleneck; each stream's S load / scale / max / O rescale runs during
-        // the other's exp phase (named barriers 1 = "A may exp", 2 = "B may exp")
-        if (kTurns && pair2) ptx::named_bar_sync(1 + x, 256);
+        // exp phases of the two streams alternate when kTurns (named barriers 1 = "A may
+        // exp", 2 = "B may exp"): MUFU.EX2 is the shared bottleneck
+        if (kTurns && pair2) ptx::named_bar_sync(1 + x, 256 * kSplit);
+        TRACE(tw, x, 4);
         PROF_MARK(5);
+        // exp2 + E4M3 requantisation of P, software-pipelined: the 32 MUFU.EX2 of key
+        // group q are interleaved with the F2FP packs of group q - 1
         const float2 rf2 = make_float2(rowf, rowf), b2 = make_float2(bias, bias);
         float2 ls = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {  // 32 keys = 8 P words per tcgen05.st
-          uint32_t pk[8];
-#pragma unroll
-          for (int w = 0; w < 8; ++w) {
-            const int k4 = 32 * q4 + 4 * w;
-            float2 x0 = __ffma2_rn(make_float2(tv[k4], tv[k4 + 1]), rf2, b2);
-            float2 x1 = __ffma2_rn(make_float2(tv[k4 + 2], tv[k4 + 3]), rf2, b2);
-            x0.x = fast_exp2(x0.x);
-            x0.y = fast_exp2(x0.y);
-            x1.x = fast_exp2(x1.x);
-            x1.y = fast_exp2(x1.y);
-            const float2 s01 = __fadd2_rn(x0, x1);
-            ls = (q4 == 0 && w == 0) ? s01 : __fadd2_rn(ls, s01);
-            pk[w] = static_cast<uint32_t>(ptx::cvt_e4m3x2(x0.x, x0.y)) |
-                    (static_cast<uint32_t>(ptx::cvt_e4m3x2(x1.x, x1.y)) << 16);
-          }
-          ptx::tmem_st8(tmem + C::tP(x) + lane_base + 8 * q4, pk);
+        for (int k2 = 0; k2 < NK; k2 += 2) {
+          const float2 v = __ffma2_rn(make_float2(tv[k2], tv[k2 + 1]), rf2, b2);
+          tv[k2] = v.x;
+          tv[k2 + 1] = v.y;
         }
-        if (kTurns && pair2) ptx::named_bar_arrive(2 - x, 256);
+        uint32_t pk[8];
+#pragma unroll
+        for (int q4 = 0; q4 <= NG; ++q4) {  // key group q4 = keys kb + [32 q4, 32 q4 + 32)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (q4 < NG) {
+              const int kk = 32 * q4 + 2 * j;
+              if ((j & 3) < kPolyPP) {  // FMA-pipe exp2 for a fixed share of the pairs (offloads MUFU)
+                const float2 e2 = exp2_poly2(make_float2(tv[kk], tv[kk + 1]));
+                tv[kk] = e2.x;
+                tv[kk + 1] = e2.y;
+              } else {
+                tv[kk] = exp2_ordered(tv[kk]);
+                tv[kk + 1] = exp2_ordered(tv[kk + 1]);
+              }
+            }
+            if (q4 > 0) {
+              const int kk = 32 * (q4 - 1) + 2 * j;  // pack P of group q4 - 1
+              const uint32_t hv = cvt_e4m3x2_ordered(tv[kk], tv[kk + 1]);
+              if (j & 1) {
+                pk[j >> 1] |= hv << 16;
+              } else {
+                pk[j >> 1] = hv;
+              }
+              const float2 e2 = make_float2(tv[kk], tv[kk + 1]);
+              ls = (q4 == 1 && j == 0) ? e2 : __fadd2_rn(ls, e2);
+            }
+          }
+          if (q4 > 0) ptx::tmem_st8(tmem + C::tP(x) + lane_base + NW * hh + 8 * (q4 - 1), pk);
+        }
+        if (kTurns && pair2) ptx::named_bar_arrive(2 - x, 256 * kSplit);
+        TRACE(tw, x, 5);
         l2 = __ffma2_rn(l2, make_float2(alpha, alpha), ls);
         PROF_MARK(6);
         if (e > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
-          // O row *= alpha
+          // this thread's O columns *= alpha
           const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
-          for (int cq = 0; cq < DV / 32; ++cq) {
-            const uint32_t ta = tmem + C::tO(x) + lane_base + 32 * cq;
+          for (int cq = 0; cq < OC / 32; ++cq) {
+            const uint32_t ta = tmem + C::tO(x) + lane_base + OC * hh + 32 * cq;
             uint32_t rr[32];
             ptx::tmem_ld32(ta, rr);
             ptx::tmem_ld_wait();
@@ -670,20 +780,27 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(p_full + x);
+        TRACE(tw, x, 6);
         PROF_MARK(7);
       }
 
       // ---- epilogue: O / l (attention.py:104-106), one row per thread (32x32b)
-      const float my_l = l2.x + l2.y;
+      float my_l = l2.x + l2.y;
+      if (kSplit == 2) {
+        float* rl = red + 1024 + ((it & 1) * 2 + x) * 256;
+        rl[hh * 128 + row] = my_l;
+        ptx::named_bar_sync(xbar, 64);
+        my_l += rl[(hh ^ 1) * 128 + row];
+      }
       const float inv_l = 1.0f / (my_l > 0.f ? my_l : 1.0f);
       if (plan.n > 0) {
         ptx::mbar_wait(o_done + x, (g - 1) & 1);
         ptx::tc_fence_after();
       }
-      const uint32_t tO = tmem + C::tO(x) + lane_base;
+      const uint32_t tO = tmem + C::tO(x) + lane_base + OC * hh;
       const int64_t orow = static_cast<int64_t>(my_bh) * p.lq + qrow;
 #pragma unroll
-      for (int c = 0; c < DV / 32; ++c) {
+      for (int c = 0; c < OC / 32; ++c) {
         uint32_t rr[32];
         if (plan.n > 0) {
           ptx::tmem_ld32(tO + 32 * c, rr);
@@ -692,250 +809,12 @@ __global__ void __launch_bounds__(384, 1) dma_attn_pp_kernel(const __grid_consta
 #pragma unroll
           for (int i2 = 0; i2 < 32; ++i2) rr[i2] = 0u;
         }
-        if (qrow < p.lq) store_orow<DV>(p, orow, c, rr, inv_l);
+        if (qrow < p.lq) store_orow<DV>(p, orow, (OC / 32) * hh + c, rr, inv_l);
       }
       ptx::tc_fence_before();
       PROF_MARK(8);
     }
-    if (kTurns && x == 0) ptx::named_bar_sync(1, 256);  // consume B's last hand-over
-    PROF_FLUSH(0, 10);
-  } else {
-    ptx::setmaxnreg_inc<216>();  // the 128-value S fragment stays in registers
-    // =========================== softmax (one warpgroup per stream) ===========================
-    // TMEM is read in the 16x256b shape: thread (r0 = lane/4, m = lane%4) of a warp
-    // holds rows quad*32 + r0 + 8i (i = 0..3) and the 32 S columns 8g + 2m + b.
-    // K rows are permuted inside every 128-key tile (quant.cuh, kPermKeys) so that
-    // these 32 columns are exactly the keys 32g' + 8m + (0..7) whose E4M3 P bytes
-    // form the P words this thread owns in the same shape: no shuffles for P,
-    // and only 32 (not 128) S_q^K factors per thread per tile.
-    const int x = warp >> 2;  // stream
-    const int quad = warp & 3;
-    const int m4 = lane & 3, r0 = lane >> 2;
-    const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
-    constexpr uint32_t kHalf = 16u << 16;  // lane offset of the second 16-lane block
-    // Lazy rescaling (the FA4 trick): a row keeps its running max until a tile
-    // raises it by more than kLazy (log2 units), so O is rarely rescaled.  P can
-    // then reach 2^kLazy and is stored as E4M3(P * 2^(8 - kLazy)) <= 256 < 448.
-    constexpr float kLazy = 4.f;
-    constexpr float kPShift = 8.f - kLazy;
-    uint32_t g = 0, sc = 0;                // this stream's tile ordinal / S_q^K ring counter
-    if (kTurns && x == 1) ptx::named_bar_arrive(1, 256);  // A takes the first exp phase
-    PROF_DECL
-
-    for (uint32_t it = 0;; ++it) {
-      const int ss = it % C::kNSch;
-      ptx::mbar_wait(sch_full + ss, (it / C::kNSch) & 1);
-      const int k = sched[ss];
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(sch_empty + ss);
-      if (k < 0) break;
-      int bh[2], qt;
-      pair_coords(p, pp, k, bh[0], bh[1], qt);
-      const int my_bh = bh[x];
-      Plan plan;
-      plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
-      if (my_bh < 0) continue;  // odd head count: stream B idles on this pair
-      const bool pair2 = bh[1] >= 0;
-      const int q0 = qt * C::kBM;
-      int qrow[4];
-      float sq_q[4], m_run[4], l_run[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        qrow[i] = q0 + quad * 32 + r0 + 8 * i;
-        sq_q[i] = (qrow[i] < p.lq) ? p.qs_q[static_cast<int64_t>(my_bh) * p.lq_pad + qrow[i]] : 1.0f;
-        m_run[i] = -INFINITY;
-        l_run[i] = 0.f;
-      }
-
-      for (int e = 0; e < plan.n; ++e, ++g) {
-        int t;
-        bool hi;
-        plan.entry(e, t, hi);
-        if (LOW == kLowHigh) hi = true;
-        const bool two_level = hi || (LOW == kLowNV);
-        const int k0 = t * C::kBN;
-        PROF_MARK(9);
-        ptx::mbar_wait(s_full + x, g & 1);
-        ptx::tc_fence_after();
-        PROF_MARK(0);
-        // S fragment, loaded in place: s[64 (i / 2) + 4 g + 2 (i % 2) + b] = S[row i][col 8g + 2m + b]
-        float s[128];
-        ptx::tmem_ld_16x256b_x16(tmem + C::tS + lane_base, *reinterpret_cast<uint32_t(*)[64]>(&s[0]));
-        ptx::tmem_ld_16x256b_x16(tmem + C::tS + lane_base + kHalf, *reinterpret_cast<uint32_t(*)[64]>(&s[64]));
-        ptx::tmem_ld_wait();
-#define SIDX(i, gg, b) (64 * ((i) >> 1) + 4 * (gg) + 2 * ((i) & 1) + (b))
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(s_free);  // S buffer may be overwritten by the next QK
-        PROF_MARK(1);
-        {
-          const int sl = sc % C::kNS;
-          ++sc;
-          if (two_level) {
-            // this thread's 32 factors are contiguous: [36 m + 2 g + b]
-            const uint32_t sqk = ptx::smem_u32(smem + C::oSqK + (x * C::kNS + sl) * C::kSqkBytes) + 144 * m4;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {  // factors for columns g = 2j, 2j + 1
-              const float4 f = ptx::lds_f4(sqk + 16 * j);
-              const float2 f0 = make_float2(f.x, f.y), f1 = make_float2(f.z, f.w);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const float2 a = __fmul2_rn(make_float2(s[SIDX(i, 2 * j, 0)], s[SIDX(i, 2 * j, 1)]), f0);
-                const float2 b = __fmul2_rn(make_float2(s[SIDX(i, 2 * j + 1, 0)], s[SIDX(i, 2 * j + 1, 1)]), f1);
-                s[SIDX(i, 2 * j, 0)] = a.x;
-                s[SIDX(i, 2 * j, 1)] = a.y;
-                s[SIDX(i, 2 * j + 1, 0)] = b.x;
-                s[SIDX(i, 2 * j + 1, 1)] = b.y;
-              }
-            }
-          }
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(sq_empty + x * C::kNS + sl);
-        }
-        PROF_MARK(2);
-        // causal (attention.py:178-184, applied when k1-1 > q0, :306) and ragged-key masks;
-        // column 8g + 2m + b holds key k0 + 32(g/4) + 8m + 2(g%4) + b
-        const int kvalid = p.lk - k0;
-        const bool need_causal = p.causal && (k0 + (kvalid < C::kBN ? kvalid : C::kBN) - 1 > q0);
-        if (need_causal || kvalid < C::kBN) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int lim = need_causal ? min(qrow[i] - k0 + 1, kvalid) : kvalid;
-#pragma unroll
-            for (int gg = 0; gg < 16; ++gg)
-#pragma unroll
-              for (int b = 0; b < 2; ++b)
-                if (32 * (gg >> 2) + 8 * m4 + 2 * (gg & 3) + b >= lim) s[SIDX(i, gg, b)] = -INFINITY;
-          }
-        }
-        float rowf[4], bias[4], alpha[4];
-        bool any_alpha = false;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float mx = fmaxf(s[SIDX(i, 0, 0)], s[SIDX(i, 0, 1)]);
-#pragma unroll
-          for (int gg = 1; gg < 16; ++gg) mx = ptx::fmax3(mx, s[SIDX(i, gg, 0)], s[SIDX(i, gg, 1)]);
-          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-          rowf[i] = two_level ? sq_q[i] : 1.0f;
-          const float m_cand = fmaxf(m_run[i], mx * rowf[i]);
-          const bool upd = m_cand > m_run[i] + kLazy;  // always for the first live tile (m_run = -inf)
-          const float m_new = upd ? m_cand : m_run[i];
-          const bool dead = (m_new == -INFINITY);
-          alpha[i] = (dead || !upd) ? 1.0f : fast_exp2(m_run[i] - m_new);  // m_run = -inf -> 0
-          bias[i] = dead ? 0.f : (kPShift - m_new);
-          m_run[i] = m_new;
-          any_alpha |= alpha[i] != 1.0f;
-        }
-        PROF_MARK(3);
-        // P_x (and O_x) are read by PV(e-1): wait for it before overwriting
-        if (e > 0) {
-          ptx::mbar_wait(o_done + x, (g - 1) & 1);
-          ptx::tc_fence_after();
-        }
-        PROF_MARK(4);
-        // exp phases of the two streams alternate (A, B, A, B, ...): MUFU.EX2 is the
-        // shared bottleneck; each stream's loads / max / O rescale run during the
-        // other's exp phase (named barriers 1 = "A may exp", 2 = "B may exp")
-        if (kTurns && pair2) ptx::named_bar_sync(1 + x, 256);
-        PROF_MARK(5);
-#pragma unroll
-        for (int blk = 0; blk < 2; ++blk) {  // rows 2 blk, 2 blk + 1 (one 16-lane TMEM block)
-          uint32_t pk[16];  // st.16x256b.x4: rep G -> {row 2blk: word 8G+2m, 8G+2m+1; row 2blk+1: same}
-#pragma unroll
-          for (int ii = 0; ii < 2; ++ii) {
-            const int i = 2 * blk + ii;
-            const float2 rf2 = make_float2(rowf[i], rowf[i]), b2 = make_float2(bias[i], bias[i]);
-            float2 ls = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int G = 0; G < 4; ++G) {
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {  // word h of rep G = keys of columns g = 4G + 2h, 4G + 2h + 1
-                const int gg = 4 * G + 2 * h;
-                float2 x0 = __ffma2_rn(make_float2(s[SIDX(i, gg, 0)], s[SIDX(i, gg, 1)]), rf2, b2);
-                float2 x1 = __ffma2_rn(make_float2(s[SIDX(i, gg + 1, 0)], s[SIDX(i, gg + 1, 1)]), rf2, b2);
-                x0.x = fast_exp2(x0.x);
-                x0.y = fast_exp2(x0.y);
-                x1.x = fast_exp2(x1.x);
-                x1.y = fast_exp2(x1.y);
-                ls = __fadd2_rn(ls, __fadd2_rn(x0, x1));
-                pk[4 * G + 2 * ii + h] = static_cast<uint32_t>(ptx::cvt_e4m3x2(x0.x, x0.y)) |
-                                         (static_cast<uint32_t>(ptx::cvt_e4m3x2(x1.x, x1.y)) << 16);
-              }
-            }
-            l_run[i] = fmaf(l_run[i], alpha[i], ls.x + ls.y);
-          }
-          ptx::tmem_st_16x256b_x4(tmem + C::tP(x) + lane_base + (blk ? kHalf : 0u), pk);
-        }
-#undef SIDX
-        if (kTurns && pair2) ptx::named_bar_arrive(2 - x, 256);
-        PROF_MARK(6);
-        if (e > 0 && __any_sync(0xffffffffu, any_alpha)) {
-          // O rows (same 16x256b ownership as S / P) *= alpha
-#pragma unroll
-          for (int blk = 0; blk < 2; ++blk) {
-            const float2 a0 = make_float2(alpha[2 * blk], alpha[2 * blk]);
-            const float2 a1 = make_float2(alpha[2 * blk + 1], alpha[2 * blk + 1]);
-#pragma unroll
-            for (int cq = 0; cq < DV / 32; ++cq) {
-              const uint32_t ta = tmem + C::tO(x) + lane_base + (blk ? kHalf : 0u) + 32 * cq;
-              uint32_t rr[16];
-              ptx::tmem_ld_16x256b_x4(ta, rr);
-              ptx::tmem_ld_wait();
-#pragma unroll
-              for (int G = 0; G < 4; ++G) {
-                const float2 u = __fmul2_rn(make_float2(__uint_as_float(rr[4 * G]), __uint_as_float(rr[4 * G + 1])), a0);
-                const float2 v = __fmul2_rn(make_float2(__uint_as_float(rr[4 * G + 2]), __uint_as_float(rr[4 * G + 3])), a1);
-                rr[4 * G] = __float_as_uint(u.x);
-                rr[4 * G + 1] = __float_as_uint(u.y);
-                rr[4 * G + 2] = __float_as_uint(v.x);
-                rr[4 * G + 3] = __float_as_uint(v.y);
-              }
-              ptx::tmem_st_16x256b_x4(ta, rr);
-            }
-          }
-        }
-        ptx::tmem_st_wait();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(p_full + x);
-        PROF_MARK(7);
-      }
-
-      // ---- epilogue: O / l (attention.py:104-106), one row per thread (32x32b)
-      float my_l = 0.f;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float l = l_run[i];
-        l += __shfl_xor_sync(0xffffffffu, l, 1);
-        l += __shfl_xor_sync(0xffffffffu, l, 2);
-        const float v = __shfl_sync(0xffffffffu, l, 4 * (lane & 7));  // row (lane & 7) + 8 i
-        if ((lane >> 3) == i) my_l = v;
-      }
-      const float inv_l = 1.0f / (my_l > 0.f ? my_l : 1.0f);
-      if (plan.n > 0) {
-        ptx::mbar_wait(o_done + x, (g - 1) & 1);
-        ptx::tc_fence_after();
-      }
-      const int orow_q = q0 + quad * 32 + lane;
-      const uint32_t tO = tmem + C::tO(x) + lane_base;
-      const int64_t orow = static_cast<int64_t>(my_bh) * p.lq + orow_q;
-#pragma unroll
-      for (int c = 0; c < DV / 32; ++c) {
-        uint32_t rr[32];
-        if (plan.n > 0) {
-          ptx::tmem_ld32(tO + 32 * c, rr);
-          ptx::tmem_ld_wait();
-        } else {
-#pragma unroll
-          for (int i2 = 0; i2 < 32; ++i2) rr[i2] = 0u;
-        }
-        if (orow_q < p.lq) store_orow<DV>(p, orow, c, rr, inv_l);
-      }
-      ptx::tc_fence_before();
-      PROF_MARK(8);
-    }
-    if (kTurns && x == 0) ptx::named_bar_sync(1, 256);  // consume B's last hand-over
+    if (kTurns && x == 0) ptx::named_bar_sync(1, 256 * kSplit);  // consume B's last hand-over
     PROF_FLUSH(0, 10);
   }
 

@@ -268,7 +268,7 @@ static int launch_pp(const AttnParams& p, const PPParams& q, cudaStream_t st) {
   static_assert(C::kSmemBytes <= 227 * 1024, "smem budget");
   DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
   const int grid = q.n_pairs < num_sms() ? q.n_pairs : num_sms();
-  kern<<<static_cast<unsigned>(grid), 384, C::kSmemBytes, st>>>(p, q);
+  kern<<<static_cast<unsigned>(grid), C::kThreads, C::kSmemBytes, st>>>(p, q);
   DMA_LAUNCH_CHECK();
   ++g_launches;
   return 0;
@@ -393,6 +393,16 @@ int dma_attention_fwd(const DmaAttnArgs* a, void* stream) {
 
 int dma_last_launch_count(void) { return g_launches; }
 
+#ifdef DMA_TRACE
+// tracing builds only: copy out and clear the CTA-0 event trace ([4][4096] + counts)
+int dma_trace_read(unsigned long long* out, unsigned int* counts) {
+  DMA_CUDA_TRY(cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 4 * 4096));
+  DMA_CUDA_TRY(cudaMemcpyFromSymbol(counts, g_trace_n, sizeof(unsigned int) * 4));
+  static const unsigned int z[4] = {0, 0, 0, 0};
+  DMA_CUDA_TRY(cudaMemcpyToSymbol(g_trace_n, z, sizeof(z)));
+  return 0;
+}
+#endif
 #ifdef DMA_PROFILE
 // profiling builds only: copy out and clear the softmax phase timers
 int dma_prof_read(unsigned long long* out, int n) {

@@ -4,6 +4,7 @@
 // cute/arch/mma_sm100_desc.hpp, which we only read as documentation).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace dma {
@@ -55,7 +56,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
+#ifdef DMA_DEBUG_WAITS
+    if (clock64() - t0 > (1ll << 36)) {  // deadlock guard (~35 s): say which barrier, then fail loudly
+      if ((threadIdx.x & 31) == 0)
+        printf("dma: mbarrier wait timeout: block %d warp %d smem 0x%x parity %u\n", blockIdx.x, threadIdx.x >> 5,
+               smem_u32(bar), parity);
+      __trap();
+    }
+#else
     if (clock64() - t0 > (1ll << 36)) __trap();  // deadlock guard (~35 s): fail loudly, never hang
+#endif
   }
 }
 
