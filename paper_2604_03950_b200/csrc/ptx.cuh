@@ -52,6 +52,13 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifdef DMA_DEBUG_WAITS
+// per-CTA progress words of the roles (MMA, producer, softmax A, softmax B), printed on a wait timeout
+__device__ volatile unsigned int dbg_progress[4 * 1024];
+#define DMA_PROGRESS(role, v) do { if ((threadIdx.x & 31) == 0) ::dma::ptx::dbg_progress[blockIdx.x * 4 + (role)] = (v); } while (0)
+#else
+#define DMA_PROGRESS(role, v) do {} while (0)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
@@ -59,8 +66,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #ifdef DMA_DEBUG_WAITS
     if (clock64() - t0 > (1ll << 36)) {  // deadlock guard (~35 s): say which barrier, then fail loudly
       if ((threadIdx.x & 31) == 0)
-        printf("dma: mbarrier wait timeout: block %d warp %d smem 0x%x parity %u\n", blockIdx.x, threadIdx.x >> 5,
-               smem_u32(bar), parity);
+        printf("dma: mbarrier wait timeout: block %d warp %d smem 0x%x parity %u  progress %08x %08x %08x %08x\n",
+               blockIdx.x, threadIdx.x >> 5, smem_u32(bar), parity, dbg_progress[blockIdx.x * 4],
+               dbg_progress[blockIdx.x * 4 + 1], dbg_progress[blockIdx.x * 4 + 2], dbg_progress[blockIdx.x * 4 + 3]);
       __trap();
     }
 #else
@@ -406,6 +414,61 @@ DMA_WU_MMA(mma_mxf8f6f4_ts, "kind::mxf8f6f4.block_scale.scale_vec::1X", "[%1]", 
 DMA_WU_MMA(mma_nvf4, "kind::mxf4nvf4.block_scale.scale_vec::4X", "%1", "l", uint64_t)
 DMA_WU_MMA(mma_mxf4, "kind::mxf4.block_scale.scale_vec::2X", "%1", "l", uint64_t)
 #undef DMA_WU_MMA
+
+// Two chained block-scaled MMAs (K chunks 0 and 1 of one tile) + a commit, from one
+// elected lane in one asm block: the second MMA's smem descriptors are the first's +
+// dstep (16-byte units), its A/B scale-factor columns + sfstep; idesc1 may differ
+// (scale-factor id).  acc0 = accumulate flag of the first MMA (the second accumulates).
+#define DMA_WU_MMA2(name, kind_str, a_operand, a_constraint, a_type, a_add)                                  \
+  __device__ __forceinline__ void name(uint32_t d, a_type a, uint64_t bdesc, uint32_t idesc0, uint32_t idesc1, \
+                                       uint32_t sfa, uint32_t sfb, uint32_t sfstep, uint32_t acc0, uint64_t bstep,\
+                                       uint64_t* bar) {                                                        \
+    asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b64 b1;\n\t.reg .b32 sa1, sb1;\n\t"                          \
+                 a_add                                                                                         \
+                 "add.s64 b1, %2, %10;\n\tadd.u32 sa1, %5, %7;\n\tadd.u32 sb1, %6, %7;\n\t"                   \
+                 "setp.ne.b32 p, %8, 0;\n\t" DMA_WU_ELECT                                                      \
+                 "@e tcgen05.mma.cta_group::1." kind_str " [%0], " a_operand ", %2, %3, [%5], [%6], p;\n\t"    \
+                 "@e tcgen05.mma.cta_group::1." kind_str " [%0], a1, b1, %4, [sa1], [sb1], 1;\n\t"              \
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t}"         \
+                 ::"r"(d), a_constraint(a), "l"(bdesc), "r"(idesc0), "r"(idesc1), "r"(sfa), "r"(sfb),          \
+                   "r"(sfstep), "r"(acc0), "r"(smem_u32(bar)), "l"(bstep)                                      \
+                 : "memory");                                                                                  \
+  }
+// A from shared memory: the second A descriptor is the first + bstep as well
+DMA_WU_MMA2(mma2_nvf4_commit, "kind::mxf4nvf4.block_scale.scale_vec::4X", "%1", "l", uint64_t,
+            ".reg .b64 a1;\n\tadd.s64 a1, %1, %10;\n\t")
+DMA_WU_MMA2(mma2_mxf4_commit, "kind::mxf4.block_scale.scale_vec::2X", "%1", "l", uint64_t,
+            ".reg .b64 a1;\n\tadd.s64 a1, %1, %10;\n\t")
+#undef DMA_WU_MMA2
+
+// PV: two MXFP8 MMAs with A = P from TMEM (second A block 8 columns on), B = V (MN-major,
+// second block bstep further), V scale factors with sf ids in idesc0 / idesc1, then a
+// commit when bar != nullptr
+template <bool kCommit>
+__device__ __forceinline__ void mma2_f8ts_impl(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc0,
+                                               uint32_t idesc1, uint32_t sfa, uint32_t sfb, uint32_t acc0,
+                                               uint64_t bstep, uint64_t* bar) {
+  asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b64 b1;\n\t.reg .b32 a1;\n\t"
+               "add.u32 a1, %1, 8;\n\tadd.s64 b1, %2, %9;\n\t"
+               "setp.ne.b32 p, %7, 0;\n\t" DMA_WU_ELECT
+               "@e tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale.scale_vec::1X [%0], [%1], %2, %3, [%5], [%6], p;\n\t"
+               "@e tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale.scale_vec::1X [%0], [a1], b1, %4, [%5], [%6], 1;\n\t"
+               "}"
+               ::"r"(d), "r"(a_tmem), "l"(bdesc), "r"(idesc0), "r"(idesc1), "r"(sfa), "r"(sfb), "r"(acc0),
+                 "r"(0), "l"(bstep)
+               : "memory");
+  if (kCommit) tc_commit(bar);
+}
+__device__ __forceinline__ void mma2_f8ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc0,
+                                          uint32_t idesc1, uint32_t sfa, uint32_t sfb, uint32_t acc0,
+                                          uint64_t bstep) {
+  mma2_f8ts_impl<false>(d, a_tmem, bdesc, idesc0, idesc1, sfa, sfb, acc0, bstep, nullptr);
+}
+__device__ __forceinline__ void mma2_f8ts_commit(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc0,
+                                                 uint32_t idesc1, uint32_t sfa, uint32_t sfb, uint32_t acc0,
+                                                 uint64_t bstep, uint64_t* bar) {
+  mma2_f8ts_impl<true>(d, a_tmem, bdesc, idesc0, idesc1, sfa, sfb, acc0, bstep, bar);
+}
 }  // namespace wu
 
 // Low word of a UMMA smem descriptor for a 16-B aligned shared address below 256 KB:

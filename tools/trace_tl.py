@@ -52,17 +52,18 @@ for x in (0, 1):
     for key, vals in sorted(d.items()):
         if len(vals) > 10:
             print(f"  {names.get(key[0])} -> {names.get(key[1])}: median {np.median(vals):.0f} cyc  (n={len(vals)})")
-e = ev[2]
-dm = {}
-for (t1, a1), (t2, a2) in zip(e, e[1:]):
-    dm.setdefault((a1, a2), []).append(t2 - t1)
-print("MMA issuer:")
-for key, vals in sorted(dm.items()):
-    if len(vals) > 10:
-        print(f"  {names.get(key[0])} -> {names.get(key[1])}: median {np.median(vals):.0f} cyc  (n={len(vals)})")
+for r in (2, 3):
+    e = ev[r]
+    dm = {}
+    for (t1, a1), (t2, a2) in zip(e, e[1:]):
+        dm.setdefault((a1, a2), []).append(t2 - t1)
+    print(f"role {r} (MMA issuer / producer):")
+    for key, vals in sorted(dm.items()):
+        if len(vals) > 10:
+            print(f"  {names.get(key[0])} -> {names.get(key[1])}: median {np.median(vals):.0f} cyc  (n={len(vals)})")
 # window of the interleaved timeline
-merged = sorted([(t, r, a) for r in range(3) for (t, a) in ev[r]])
+merged = sorted([(t, r, a) for r in range(4) for (t, a) in ev[r]])
 mid = len(merged) // 2
 print("timeline (cycles since start):")
 for t, r, a in merged[mid:mid + 40]:
-    print(f"  {t:10d} {['A', 'B', 'MMA'][r]:>3s} {names.get(a, a)}")
+    print(f"  {t:10d} {['A', 'B', 'MMA', 'MMA2'][r]:>4s} {names.get(a, a)}")
