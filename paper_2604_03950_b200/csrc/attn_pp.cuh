@@ -84,6 +84,10 @@ __device__ unsigned int g_trace_n[4];
 // polynomial (exp2_poly2) instead of MUFU.EX2
 constexpr int kPolyPP = DMA_PP_POLY;
 
+#ifndef DMA_PP_EARLY_FREE
+#define DMA_PP_EARLY_FREE 0
+#endif
+
 #ifndef DMA_PP_TURNS
 #define DMA_PP_TURNS 0
 #endif
@@ -658,12 +662,21 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
             tv[4 * w + 3] = b.y;
           }
         };
+#if DMA_PP_EARLY_FREE
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(s_free);  // S buffer may be overwritten by the next QK
+        TRACE(tw, x, 2);
+        scale_words(0);
+#else
         scale_words(0);
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(s_free);  // S buffer may be overwritten by the next QK
         TRACE(tw, x, 2);
+#endif
         scale_words(NW / 2);
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(sq_empty + x * C::kNS + sl);
