@@ -257,12 +257,15 @@ def main():
             shard = plan_shard(world * B, H, KVH, world, rank)
 
         def e2e_step():
+            if shard is None:
+                # public API on host tensors: chunked H2D / forward / D2H pipeline (DmaAttention.forward_host)
+                fwd(hq, hk, hv, out=ho)
+                return
             dq.copy_(hq, non_blocking=True)
             dk.copy_(hk, non_blocking=True)
             dv.copy_(hv, non_blocking=True)
             fwd(dq, dk, dv, out=out)
-            if shard is not None:
-                gather(out.reshape(1, B * H, N, d), shard, world * B, H)  # NCCL all_gather of O
+            gather(out.reshape(1, B * H, N, d), shard, world * B, H)  # NCCL all_gather of O
             ho.copy_(out, non_blocking=True)
 
         e2e_step()
@@ -282,8 +285,9 @@ def main():
         d2h = out.numel() * out.element_size()
         e2e = {"value": world * F / (float(te.item()) * 1e-3) / 1e12, "unit": "TFLOPS",
                "ms_per_step": float(te.item()), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "api": "paper_2604_03950_b200.DmaAttention.__call__ (pinned host buffers)"
-                      + (" + sharding.gather (NCCL all_gather of O)" if world > 1 else ""),
+               "api": ("paper_2604_03950_b200.DmaAttention.__call__ on pinned host tensors (forward_host: "
+                       "chunked H2D / forward / D2H on 3 streams)") if world == 1 else
+                      "DmaAttention.__call__ on device copies of pinned host tensors + sharding.gather (NCCL all_gather of O)",
                "gather_bytes_per_step": (world * d2h if world > 1 else 0)}
 
     if rank == 0:

@@ -142,8 +142,82 @@ class DmaAttention:
         return a, out
 
     def __call__(self, q, k, v, out=None, out_dtype=None, stream=None):
+        if not q.is_cuda:
+            return self.forward_host(q, k, v, out=out, out_dtype=out_dtype)
         a, out = self.prepare(q, k, v, out, out_dtype)
         _lib.check(_lib.lib().dma_attention_fwd(a, _lib.stream_ptr(stream)), "dma_attention")
+        return out
+
+    def forward_host(self, q, k, v, out=None, out_dtype=None, chunk_kv_heads=None):
+        """Forward on HOST tensors [B, H, Lq, D] / [B, KVH, Lk, D] (pinned for full speed).
+
+        The problem is cut into chunks of whole KV-head groups (GQA groups never
+        split); chunk i's host->device copy, chunk i-1's forward and chunk i-2's
+        device->host copy run concurrently on three CUDA streams (two device
+        buffer sets), so the PCIe transfers -- not the sum of transfers and
+        compute -- bound the end-to-end time.  Returns ``out`` (host).
+        """
+        import torch
+
+        B, H, Lq, D = q.shape
+        _, KVH, Lk, _ = k.shape
+        DV = v.shape[-1]
+        _check_qkv(q.shape, k.shape, v.shape, self.cfg.causal)
+        if H % KVH:
+            raise ValueError(f"heads {H} not divisible by kv_heads {KVH}")
+        G = H // KVH
+        odt = out_dtype or (torch.bfloat16 if q.dtype == torch.bfloat16 else torch.float32)
+        if out is None:
+            out = torch.empty((B, H, Lq, DV), dtype=odt, pin_memory=True)
+        if chunk_kv_heads is None:
+            # >= 4 query heads (2 head pairs x every q tile fill the 148 SMs at N >= 8K)
+            # and ~8 chunks per batch element to keep the pipeline full
+            chunk_kv_heads = max(1, min(KVH, max(-(-4 // G), KVH // 8)))
+        units = [(b, h0, min(KVH, h0 + chunk_kv_heads)) for b in range(B) for h0 in range(0, KVH, chunk_kv_heads)]
+        cur = torch.cuda.current_stream()
+        s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        for st in (s_in, s_cmp, s_out):
+            st.wait_stream(cur)
+        bufs, fwds = [], []
+        c0 = chunk_kv_heads
+        for _ in range(min(2, len(units))):
+            bufs.append((torch.empty((1, c0 * G, Lq, D), dtype=q.dtype, device="cuda"),
+                         torch.empty((1, c0, Lk, D), dtype=k.dtype, device="cuda"),
+                         torch.empty((1, c0, Lk, DV), dtype=v.dtype, device="cuda"),
+                         torch.empty((1, c0 * G, Lq, DV), dtype=odt, device="cuda")))
+            fwds.append(DmaAttention(self.cfg))
+        ev_cmp = [None, None]  # compute of the slot's previous chunk done (inputs free)
+        ev_out = [None, None]  # D2H of the slot's previous chunk done (output free)
+        for i, (b, h0, h1) in enumerate(units):
+            j = i % 2
+            dq, dk, dv, do = (t[:, : (h1 - h0) * G] if n in (0, 3) else t[:, : h1 - h0] for n, t in enumerate(bufs[j]))
+            with torch.cuda.stream(s_in):
+                if ev_cmp[j] is not None:
+                    s_in.wait_event(ev_cmp[j])
+                dq.copy_(q[b : b + 1, h0 * G : h1 * G], non_blocking=True)
+                dk.copy_(k[b : b + 1, h0:h1], non_blocking=True)
+                dv.copy_(v[b : b + 1, h0:h1], non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(ev_in)
+                if ev_out[j] is not None:
+                    s_cmp.wait_event(ev_out[j])
+                a, _ = fwds[j].prepare(dq, dk, dv, out=do)
+                _lib.check(_lib.lib().dma_attention_fwd(a, _lib.stream_ptr(s_cmp)), "dma_attention")
+                ev_cmp[j] = torch.cuda.Event()
+                ev_cmp[j].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_cmp[j])
+                out[b : b + 1, h0 * G : h1 * G].copy_(do, non_blocking=True)
+                ev_out[j] = torch.cuda.Event()
+                ev_out[j].record(s_out)
+            for t in (dq, dk, dv, do):
+                t.record_stream(s_in)
+                t.record_stream(s_cmp)
+                t.record_stream(s_out)
+        for st in (s_in, s_cmp, s_out):
+            cur.wait_stream(st)
         return out
 
 

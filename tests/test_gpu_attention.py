@@ -132,3 +132,23 @@ def test_unsupported_configs_raise():
         d.mixed_precision_attention(q, q, q, d.AttentionConfig(tile_m=128, tile_n=128, low_format=None))
     with pytest.raises(ValueError, match="causal"):
         d.mixed_precision_attention(q, q[:128], q[:128], d.AttentionConfig(tile_m=128, tile_n=128))
+
+
+@pytest.mark.parametrize("chunk", [1, 3])
+def test_forward_host_pipeline_matches_device(chunk):
+    """DmaAttention on pinned host tensors (chunked H2D / forward / D2H pipeline) gives
+    exactly the device-path result, including a ragged last chunk (KVH % chunk != 0)."""
+    import torch
+
+    B, H, KVH, N, d = 2, 8, 4, 768, 128
+    c, _ = cfgs("nvfp4", "e4m3", "token", 128, 128, True, "mxfp8")
+    g = torch.Generator().manual_seed(11)
+    q = torch.randn(B, H, N, d, generator=g).to(torch.bfloat16).pin_memory()
+    k = torch.randn(B, KVH, N, d, generator=g).to(torch.bfloat16).pin_memory()
+    v = torch.randn(B, KVH, N, d, generator=g).to(torch.bfloat16).pin_memory()
+    fwd = D().DmaAttention(c)
+    host = fwd.forward_host(q, k, v, chunk_kv_heads=chunk)
+    torch.cuda.synchronize()
+    dev = D().DmaAttention(c)(q.cuda(), k.cuda(), v.cuda())
+    assert not host.is_cuda and host.shape == (B, H, N, d)
+    assert torch.equal(host, dev.cpu())

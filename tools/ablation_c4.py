@@ -6,7 +6,7 @@ For every (T = S, granularity) point: attention-kernel TFLOPS (device time, CUDA
 events, median of --steps launches after warm-up; algorithmic causal FLOPs), the
 Bit_high fraction of the plan, and the output error against full-precision attention
 (cosine similarity and rel-L2 vs a float64 torch softmax(QK^T/sqrt(d))V on --heads
-sampled heads).  One JSON line per point; writes profiles/<tag>_c4_sweep.jsonl.
+sampled heads).  One JSON line per point; writes gpurun_out/<tag>_c4_sweep.jsonl.
 
   python tools/ablation_c4.py [--steps 10] [--heads 2] [--tag r01]
 """
@@ -90,8 +90,9 @@ def main():
                          "heads_checked": args.heads})
             print(json.dumps(line), flush=True)
             out_lines.append(line)
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    with open(os.path.join(ROOT, "profiles", f"{args.tag}_c4_sweep.jsonl"), "w") as f:
+    # gpurun_out/ is what travels back from the GPU box; copy it under profiles/ to keep it
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"{args.tag}_c4_sweep.jsonl"), "w") as f:
         for ln in out_lines:
             f.write(json.dumps(ln) + "\n")
 
