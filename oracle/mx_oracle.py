@@ -529,6 +529,45 @@ def reference_attention(q, k, v, causal=False) -> np.ndarray:
     return (p / np.where(den > 0, den, 1.0)) @ v
 
 
+def _softmax_rows(logits: np.ndarray, base2: bool) -> np.ndarray:
+    """attention.py:138-147."""
+    m = logits.max(axis=1, keepdims=True)
+    m = np.where(np.isfinite(m), m, 0.0)
+    z = logits - m
+    p = np.exp2(z) if base2 else np.exp(z)
+    p[~np.isfinite(logits)] = 0.0
+    den = p.sum(axis=1, keepdims=True)
+    return p / np.where(den > 0, den, 1.0)
+
+
+def reference_scores(q, k, causal=False) -> np.ndarray:
+    """Dense post-softmax probabilities, base e (attention.py:126-135)."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    _check_qkv(q, k, k, causal)
+    z = q @ k.T / math.sqrt(q.shape[1])
+    if causal:
+        n = q.shape[0]
+        z = np.where(np.arange(n)[:, None] >= np.arange(n)[None, :], z, -np.inf)
+    return _softmax_rows(z, base2=False)
+
+
+def mixed_precision_scores(q, k, cfg: Cfg) -> np.ndarray:
+    """Dense base-2 probabilities under the per-tile precision plan (attention.py:313-335)."""
+    ql, qh, kl, kh, _ = operands(q, k, np.asarray(k, dtype=np.float64), cfg)
+    lq, lk = ql.shape[0], kl.shape[0]
+    logits = np.full((lq, lk), -np.inf)
+    for qt in range(-(-lq // cfg.tile_m)):
+        q0, q1 = qt * cfg.tile_m, min((qt + 1) * cfg.tile_m, lq)
+        for kt, high in tile_plan(qt, lq, lk, cfg):
+            k0, k1 = kt * cfg.tile_n, min((kt + 1) * cfg.tile_n, lk)
+            blk = (qh if high else ql)[q0:q1] @ (kh if high else kl)[k0:k1].T
+            if cfg.causal:  # attention.py:178-184
+                blk = np.where(np.arange(q0, q1)[:, None] >= np.arange(k0, k1)[None, :], blk, -np.inf)
+            logits[q0:q1, k0:k1] = blk
+    return _softmax_rows(logits, base2=True)
+
+
 def high_precision_fraction(len_q, len_k, tile_m, tile_n, diag_window, sink_window, causal):
     """metrics.py:55-101 (Bit_high)."""
     cfg = Cfg(tile_m=tile_m, tile_n=tile_n, diag_window=diag_window,

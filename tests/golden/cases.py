@@ -21,3 +21,14 @@ ATTN_CASES = [
      dict(tile_m=128, tile_n=128, high_format="mxfp8_e5m2", low_format="mxfp4", diag_window=0)),
     ("dv32_c_128_d64", 128, 128, 64, 32, 23, dict(tile_m=32, tile_n=32, diag_window=32)),
 ]
+
+# (name, L, d, seed, AttentionConfig kwargs) for mixed_precision_scores
+SCORE_CASES = [
+    ("causal_nvfp4_token", 256, 64, 41, dict(tile_m=64, tile_n=64, diag_window=64, sink_window=64, causal=True)),
+    ("causal_mxfp4_block", 192, 64, 43, dict(tile_m=64, tile_n=64, diag_window=128, sink_window=0, causal=True,
+                                             low_format="mxfp4", granularity="block")),
+    ("noncausal_nvfp4_tensor", 160, 32, 45, dict(tile_m=32, tile_n=32, diag_window=64, sink_window=32,
+                                                 causal=False, granularity="tensor")),
+    ("causal_identity_low", 128, 64, 47, dict(tile_m=32, tile_n=32, diag_window=32, sink_window=0, causal=True,
+                                              low_format=None)),
+]

@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 sys.path.insert(0, "/root/reference/pkg/src")
 
-from cases import ATTN_CASES  # noqa: E402
+from cases import ATTN_CASES, SCORE_CASES  # noqa: E402
 from inputs import adversarial_rows, bf16_round, randn_bf16  # noqa: E402
 
 from mxattn import attention as A  # noqa: E402
@@ -155,6 +155,11 @@ def main():
     v = randn_bf16(33, 96, 64)
     g["refattn_causal"] = A.reference_attention(q, k, v, causal=True)
     g["refattn_full"] = A.reference_attention(q, k, v, causal=False)
+    g["refscores_causal"] = A.reference_scores(q, k, causal=True)
+    # --- mixed-precision score matrices (attention.py:313-335)
+    for name, lq, d, seed, kw in SCORE_CASES:
+        qq, kk = randn_bf16(seed, lq, d), randn_bf16(seed + 1, lq, d)
+        g[f"scores/{name}"] = A.mixed_precision_scores(qq, kk, make_cfg(kw))
     rep = M.similarity(g["refattn_causal"], g["refattn_full"])
     g["similarity"] = np.array([rep.cos_sim, rep.rel_l1, rep.abs_l1, rep.rmse, rep.psnr])
 

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from inputs import randn_bf16
-from cases import ATTN_CASES
+from cases import ATTN_CASES, SCORE_CASES
 from oracle import mx_oracle as O
 
 LOW = {"nvfp4": O.NVFP4, "mxfp4": O.MXFP4}
@@ -92,3 +92,17 @@ def test_reference_attention_and_similarity(golden):
     s = O.similarity(a, b)
     np.testing.assert_allclose([s["cos_sim"], s["rel_l1"], s["abs_l1"], s["rmse"], s["psnr"]],
                                golden["similarity"], rtol=1e-12)
+
+
+def test_reference_scores(golden):
+    q, k = randn_bf16(31, 96, 64), randn_bf16(32, 96, 64)
+    np.testing.assert_allclose(O.reference_scores(q, k, causal=True), golden["refscores_causal"], rtol=1e-12,
+                               atol=1e-15)
+
+
+@pytest.mark.parametrize("case", SCORE_CASES, ids=[c[0] for c in SCORE_CASES])
+def test_mixed_precision_scores(golden, case):
+    name, lq, d, seed, kw = case
+    q, k = randn_bf16(seed, lq, d), randn_bf16(seed + 1, lq, d)
+    np.testing.assert_allclose(O.mixed_precision_scores(q, k, oracle_cfg(kw)), golden[f"scores/{name}"],
+                               rtol=1e-12, atol=1e-15)
