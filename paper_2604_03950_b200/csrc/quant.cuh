@@ -344,33 +344,60 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
                                                       int is_query, double c,
                                                       const unsigned long long* __restrict__ tensor_absmax,
                                                       QuantOut out) {
-  const int tpr = cols >> 4;  // power of two in [2, 32]
+  // grid: x = blocks of 256 / tpr rows of one matrix, y = matrices (strided when n_mat > gridDim.y)
+  const int lg_tpr = __ffs(cols >> 4) - 1;  // tpr = cols / 16, a power of two in [2, 32]
+  const int tpr = 1 << lg_tpr;
   const int lane = threadIdx.x & 31;
-  const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t grow = gt / tpr;  // mat * rows + row
-  const int part = static_cast<int>(gt % tpr);
-  const bool live = grow < n_mat * rows;  // whole rows live or die together (tpr | 32)
+  const int part = threadIdx.x & (tpr - 1);
+  const int64_t row = (static_cast<int64_t>(blockIdx.x) << (8 - lg_tpr)) + (threadIdx.x >> lg_tpr);
+  const bool live = row < rows;  // whole rows live or die together (tpr | 32)
   if (__all_sync(0xffffffffu, !live)) return;
-  const int64_t mat = live ? grow / rows : 0, row = live ? grow % rows : 0;
+  for (int64_t mat = blockIdx.y; mat < n_mat; mat += gridDim.y) {
 
+  // Maxima use monotonicity instead of per-element f64 compares: fl(|x| c) and the
+  // correctly rounded fl(|x| / S_q) are non-decreasing in |x|, so the max of the
+  // rounded values is the rounded max (the argument quantize.py's TENSOR path
+  // already relies on).  For bf16 inputs max |x| is an integer max on the bit
+  // patterns, which also flags Inf / NaN (magnitude >= 0x7F80).
   double xs[16];
-  if (live) {
-    Load16<T>::run(x + mat * mat_stride + row * row_stride + part * 16, xs);
+  double amax;  // max |x| of this thread's 16 values (input precision, exact)
+  bool bad;
+  if constexpr (sizeof(T) == 2) {
+    uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    if (live) {
+      const uint4* src = reinterpret_cast<const uint4*>(x + mat * mat_stride + row * row_stride + part * 16);
+      const uint4 a = __ldg(src), b = __ldg(src + 1);
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    }
+    uint32_t mm = w[0] & 0x7FFF7FFFu;
+#pragma unroll
+    for (int i = 1; i < 8; ++i) mm = __vmaxu2(mm, w[i] & 0x7FFF7FFFu);
+    const uint32_t m16 = max(mm & 0xFFFFu, mm >> 16);
+    bad = m16 >= 0x7F80u;
+    amax = static_cast<double>(__uint_as_float(m16 << 16));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      xs[2 * i] = __uint_as_float(w[i] << 16);
+      xs[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
   } else {
+    if (live) {
+      Load16<T>::run(x + mat * mat_stride + row * row_stride + part * 16, xs);
+    } else {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) xs[i] = 0.0;
-  }
-  bool bad = false;
-  double amax = 0.0;
+      for (int i = 0; i < 16; ++i) xs[i] = 0.0;
+    }
+    bad = false;
+    amax = 0.0;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    bad |= (static_cast<uint32_t>(__double2hiint(xs[i])) & 0x7FF00000u) == 0x7FF00000u;  // Inf / NaN
-    if (is_query) xs[i] = __dmul_rn(xs[i], c);  // quantize.py:149 (x * c)
-    amax = fmax(amax, fabs(xs[i]));
+    for (int i = 0; i < 16; ++i) {
+      bad |= (static_cast<uint32_t>(__double2hiint(xs[i])) & 0x7FF00000u) == 0x7FF00000u;  // Inf / NaN
+      amax = fmax(amax, fabs(xs[i]));
+    }
   }
   if (out.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(out.nonfinite, 1u);
 
-  // ---- group max -> S_q (quantize.py:98-106, 152-153)
+  // ---- group max -> S_q (quantize.py:98-106, 152-153), taken on max |x| before the prescale
   double g;
   if (GRAN == DMA_GRAN_TOKEN) {
     g = shfl_max(amax, tpr);
@@ -378,21 +405,25 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
     g = shfl_max(amax, 2);
   } else {
     g = __longlong_as_double(static_cast<long long>(tensor_absmax[mat]));
-    if (is_query) g = __dmul_rn(g, c);  // max|x*c| == fl(max|x| * c): rounding is monotone
+  }
+  if (is_query) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) xs[i] = __dmul_rn(xs[i], c);  // quantize.py:149 (x * c)
+    amax = __dmul_rn(amax, c);  // = max |x * c| (monotone rounding)
+    g = __dmul_rn(g, c);
   }
   const double sq = g > 0.0 ? __ddiv_rn(g, 2688.0) : 1.0;
   const double ysq = __drcp_rn(sq);
   double xsc[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) xsc[i] = qdiv<T>(xs[i], sq, ysq);  // quantize.py:154
+  const double amax_sc = qdiv<T>(amax, sq, ysq);  // = max |x_scaled| of the 16 values
 
   // ---- 4-bit path (quantize.py:156-184)
   uint32_t packed[2] = {0u, 0u};
   uint32_t sc_low;
   if (NV) {
-    double bm = 0.0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) bm = fmax(bm, fabs(xsc[i]));
+    const double bm = amax_sc;
     uint32_t code = bm > 0.0 ? e4m3_pos(__ddiv_rn(bm, 6.0)) : 0x38u;
     if (code == 0 && bm > 0.0) code = 0x01;  // floor at 2^-9 (quantize.py:164-167)
     const double sv = decode_e4m3(code);
@@ -406,10 +437,7 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
     }
     sc_low = code;
   } else {
-    double bm = 0.0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) bm = fmax(bm, fabs(xs[i]));
-    bm = shfl_max(bm, 2);  // 32-column block = 2 lanes, single level on x_sm
+    const double bm = shfl_max(amax, 2);  // 32-column block = 2 lanes, single level on x_sm
     const int e = bm > 0.0 ? min(max(floor_log2_pos(bm) - 2, -127), 127) : -127;
     const double inv = pow2(-e);
 #pragma unroll
@@ -423,10 +451,7 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
   }
 
   // ---- 8-bit path (quantize.py:186-199)
-  double hm = 0.0;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) hm = fmax(hm, fabs(xsc[i]));
-  hm = shfl_max(hm, 2);
+  const double hm = shfl_max(amax_sc, 2);
   constexpr int kEmax = E5 ? 15 : 8;
   const int he = hm > 0.0 ? min(max(floor_log2_pos(hm) - kEmax, -127), 127) : -127;
   const double hinv = pow2(-he);
@@ -447,7 +472,7 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
     codes[j] = w;
   }
   const uint32_t sc_high = static_cast<uint32_t>(he + 127);
-  if (!live) return;
+  if (!live) continue;  // dead rows still take part in the next matrix's shuffles
 
   const int64_t rbase = mat * rows + row;
   // operand row of the codes / scale-factor atoms (permuted inside 128-row tiles for attn_pp)
@@ -485,6 +510,7 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
         out.qs_f32[mat * out.rows_pad + row] = static_cast<float>(sq);
     }
   }
+  }  // mat loop
 }
 
 // max |x| per matrix as the bit pattern of a non-negative double (atomicMax on u64)
