@@ -27,9 +27,12 @@ static void launch_rows(const DmaQuantArgs* a, const unsigned long long* tmax, c
   const int64_t tpr = a->cols / 16;
   if (tpr <= 32 && (tpr & (tpr - 1)) == 0 && a->row_stride % 8 == 0 && a->mat_stride % 8 == 0) {
     // fast path: 16 columns per thread (cols in {32, 64, 128, 256, 512})
-    // x: blocks of 256 / tpr rows of one matrix, y: matrices
-    const int64_t bx = (a->rows * tpr + 255) / 256;
+    // grid-stride over (row block, matrix) items: y covers the matrices (<= 65535),
+    // x about 8 CTAs per SM in total so every CTA walks several row blocks (prefetching)
+    const int64_t nbx = (a->rows * tpr + 255) / 256;
     const int64_t by = a->n_mat < 65535 ? a->n_mat : 65535;
+    int64_t bx = (148 * 8 + by - 1) / by;
+    bx = bx < 1 ? 1 : (bx > nbx ? nbx : bx);
     quant16_kernel<T, NV, E5, GRAN><<<dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), 256, 0, st>>>(
         static_cast<const T*>(a->x), a->n_mat, a->rows, static_cast<int>(a->cols), a->mat_stride, a->row_stride,
         a->is_query, a->prescale, tmax, out);

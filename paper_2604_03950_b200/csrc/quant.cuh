@@ -344,15 +344,44 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
                                                       int is_query, double c,
                                                       const unsigned long long* __restrict__ tensor_absmax,
                                                       QuantOut out) {
-  // grid: x = blocks of 256 / tpr rows of one matrix, y = matrices (strided when n_mat > gridDim.y)
+  // Work item = (matrix, block of 256 / tpr rows); a CTA walks items grid-stride
+  // (x over row blocks, y over matrices) and prefetches the next item's 32 input bytes
+  // while it quantizes the current one (the kernel is latency-bound otherwise).
   const int lg_tpr = __ffs(cols >> 4) - 1;  // tpr = cols / 16, a power of two in [2, 32]
   const int tpr = 1 << lg_tpr;
   const int lane = threadIdx.x & 31;
   const int part = threadIdx.x & (tpr - 1);
-  const int64_t row = (static_cast<int64_t>(blockIdx.x) << (8 - lg_tpr)) + (threadIdx.x >> lg_tpr);
-  const bool live = row < rows;  // whole rows live or die together (tpr | 32)
-  if (__all_sync(0xffffffffu, !live)) return;
+  const int rpb = 256 >> lg_tpr;  // rows per block
+  const int64_t nbx = (rows + rpb - 1) / rpb;
+  const int rsub = threadIdx.x >> lg_tpr;
+  uint4 pf0 = make_uint4(0u, 0u, 0u, 0u), pf1 = pf0;  // prefetched words (bf16 inputs)
+  auto fetch = [&](int64_t m, int64_t b) {
+    const int64_t r = b * rpb + rsub;
+    if constexpr (sizeof(T) == 2) {
+      if (m < n_mat && r < rows) {
+        const uint4* src = reinterpret_cast<const uint4*>(x + m * mat_stride + r * row_stride + part * 16);
+        pf0 = __ldg(src);
+        pf1 = __ldg(src + 1);
+      } else {
+        pf0 = pf1 = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+  };
+  fetch(blockIdx.y, blockIdx.x);
   for (int64_t mat = blockIdx.y; mat < n_mat; mat += gridDim.y) {
+  for (int64_t bx = blockIdx.x; bx < nbx; bx += gridDim.x) {
+  const int64_t row = bx * rpb + rsub;
+  const bool live = row < rows;  // whole rows live or die together (tpr | 32)
+  const uint4 cur0 = pf0, cur1 = pf1;
+  {
+    int64_t nb = bx + gridDim.x, nm = mat;
+    if (nb >= nbx) {
+      nb = blockIdx.x;
+      nm = mat + gridDim.y;
+    }
+    fetch(nm, nb);
+  }
+  if (__all_sync(0xffffffffu, !live)) continue;
 
   // Maxima use monotonicity instead of per-element f64 compares: fl(|x| c) and the
   // correctly rounded fl(|x| / S_q) are non-decreasing in |x|, so the max of the
@@ -363,12 +392,7 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
   double amax;  // max |x| of this thread's 16 values (input precision, exact)
   bool bad;
   if constexpr (sizeof(T) == 2) {
-    uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-    if (live) {
-      const uint4* src = reinterpret_cast<const uint4*>(x + mat * mat_stride + row * row_stride + part * 16);
-      const uint4 a = __ldg(src), b = __ldg(src + 1);
-      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
-    }
+    const uint32_t w[8] = {cur0.x, cur0.y, cur0.z, cur0.w, cur1.x, cur1.y, cur1.z, cur1.w};
     uint32_t mm = w[0] & 0x7FFF7FFFu;
 #pragma unroll
     for (int i = 1; i < 8; ++i) mm = __vmaxu2(mm, w[i] & 0x7FFF7FFFu);
@@ -510,7 +534,8 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
         out.qs_f32[mat * out.rows_pad + row] = static_cast<float>(sq);
     }
   }
-  }  // mat loop
+  }  // row-block loop
+  }  // matrix loop
 }
 
 // max |x| per matrix as the bit pattern of a non-negative double (atomicMax on u64)
