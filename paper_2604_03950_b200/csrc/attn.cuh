@@ -41,7 +41,10 @@
 
 namespace dma {
 
-enum LowKind { kLowNV = 0, kLowMX4 = 1, kLowHigh = 2 };
+// kLowBF16: both score operands are bf16 copies of the reference's dequantized Q / K
+// (S_q and the block scales folded in, or the identity path), QK by kind::f16 -- the
+// route for BLOCK granularity (S_q varies along the contraction) and None formats.
+enum LowKind { kLowNV = 0, kLowMX4 = 1, kLowHigh = 2, kLowBF16 = 3 };
 
 struct __align__(64) AttnParams {
   CUtensorMap tm_q_hi, tm_q_lo, tm_k_hi, tm_k_lo, tm_v;
@@ -65,14 +68,15 @@ struct __align__(64) AttnParams {
 template <int D, int DV, int LOW, bool PVBF16>
 struct AttnCfg {
   static constexpr int kBM = 128, kBN = 128;
-  static constexpr int kNQ = 2, kNK = 4, kNV = 3;
-  static constexpr int kQHiBytes = kBM * D;
-  static constexpr int kQLoBytes = kBM * D / 2;
+  static constexpr bool kBF = LOW == kLowBF16;
+  static constexpr int kNQ = kBF ? 1 : 2, kNK = kBF ? 2 : 4, kNV = kBF ? 2 : 3;
+  static constexpr int kQHiBytes = kBF ? kBM * D * 2 : kBM * D;
+  static constexpr int kQLoBytes = kBF ? kBM * D * 2 : kBM * D / 2;
   static constexpr int kQStage = ((kQHiBytes + (LOW != kLowHigh ? kQLoBytes : 0) + 1023) / 1024) * 1024;
-  static constexpr int kKBytes = kBN * D;  // fp8 size; fp4 tiles use half
+  static constexpr int kKBytes = kBF ? kBN * D * 2 : kBN * D;  // fp8 size; fp4 tiles use half
   static constexpr int kVBytes = PVBF16 ? kBN * DV * 2 : kBN * DV;
-  static constexpr int kChHi = (D / 32 + 3) / 4;
-  static constexpr int kChLo = LOW == kLowNV ? (D / 16 + 3) / 4 : (D / 32 + 3) / 4;
+  static constexpr int kChHi = kBF ? 0 : (D / 32 + 3) / 4;
+  static constexpr int kChLo = kBF ? 0 : (LOW == kLowNV ? (D / 16 + 3) / 4 : (D / 32 + 3) / 4);
   static constexpr int kChK = kChHi > kChLo ? kChHi : kChLo;
   // smem carve-up (offsets from a 1024-aligned base)
   static constexpr int oQ = 0;
@@ -89,6 +93,7 @@ struct AttnCfg {
   static constexpr int oRedL = oRed + 2 * 2 * 128 * 4;       // [2 half][128] f32 row sums
   static constexpr int oBar = oRedL + 2 * 128 * 4;
   static constexpr int kSmemBytes = oBar + 256 + 1024;       // + alignment slack
+  static_assert(kSmemBytes <= 227 * 1024, "smem budget");
   // TMEM columns
   static constexpr uint32_t tS0 = 0, tS1 = 128, tO = 256;
   static constexpr uint32_t tSfQ = 384;  // [kNQ][hi 4 | lo 8] = 24 cols
@@ -220,6 +225,15 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
         uint8_t* qdst = smem + C::oQ + qs * C::kQStage;
         uint8_t* sfq = smem + C::oSfQ + qs * C::kSfQStage;
         ptx::mbar_arrive_expect_tx(q_full + qs, qbytes);
+        if constexpr (C::kBF) {
+          // bf16 operands: 64-column (128-byte) swizzle boxes, hi then lo
+#pragma unroll
+          for (int hb = 0; hb < D / 64; ++hb) {
+            ptx::tma_load_3d(qdst + hb * (C::kBM * 128), &p.tm_q_hi, q_full + qs, hb * 64, qt * C::kBM, mat_q);
+            ptx::tma_load_3d(qdst + C::kQHiBytes + hb * (C::kBM * 128), &p.tm_q_lo, q_full + qs, hb * 64, qt * C::kBM,
+                             mat_q);
+          }
+        } else {
         ptx::tma_load_3d(qdst, &p.tm_q_hi, q_full + qs, 0, qt * C::kBM, mat_q);
         ptx::bulk_load(sfq, p.sf_q_hi + (static_cast<int64_t>(mat_q) * rt_q + qt) * p.ch_hi * 512,
                        512 * C::kChHi, q_full + qs);
@@ -227,6 +241,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
           ptx::tma_load_3d(qdst + C::kQHiBytes, &p.tm_q_lo, q_full + qs, 0, qt * C::kBM, mat_q);
           ptx::bulk_load(sfq + 512 * C::kChHi, p.sf_q_lo + (static_cast<int64_t>(mat_q) * rt_q + qt) * p.ch_lo * 512,
                          512 * C::kChLo, q_full + qs);
+        }
         }
         for (int e = 0; e < plan.n; ++e, ++kc, ++vc) {
           int t;
@@ -236,13 +251,20 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
           const int ks = kc % C::kNK;
           ptx::mbar_wait(k_empty + ks, ((kc / C::kNK) & 1) ^ 1);
           const int ch = hi ? C::kChHi : C::kChLo;
-          const uint32_t kb = hi ? C::kKBytes : C::kKBytes / 2;
+          const uint32_t kb = (hi || C::kBF) ? C::kKBytes : C::kKBytes / 2;
           ptx::mbar_arrive_expect_tx(k_full + ks, kb + 512 * ch + 512);
+          if constexpr (C::kBF) {
+#pragma unroll
+            for (int hb = 0; hb < D / 64; ++hb)
+              ptx::tma_load_3d(smem + C::oK + ks * C::kKBytes + hb * (C::kBN * 128), hi ? &p.tm_k_hi : &p.tm_k_lo,
+                               k_full + ks, hb * 64, t * C::kBN, mat_k);
+          } else {
           ptx::tma_load_3d(smem + C::oK + ks * C::kKBytes, hi ? &p.tm_k_hi : &p.tm_k_lo, k_full + ks, 0,
                            t * C::kBN, mat_k);
           const uint8_t* sfsrc = (hi ? p.sf_k_hi : p.sf_k_lo) +
                                  (static_cast<int64_t>(mat_k) * rt_k + t) * (hi ? p.ch_hi : p.ch_lo) * 512;
           ptx::bulk_load(smem + C::oSfK + ks * 512 * C::kChK, sfsrc, 512 * ch, k_full + ks);
+          }
           ptx::bulk_load(smem + C::oSqK + ks * 512, p.qs_k + static_cast<int64_t>(mat_k) * p.lk_pad + t * C::kBN,
                          512, k_full + ks);
 
@@ -322,7 +344,17 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
         const uint32_t kaddr = ptx::smem_u32(smem + C::oK + ks * C::kKBytes);
         const uint32_t qaddr = ptx::smem_u32(smem + C::oQ + qs * C::kQStage);
         const uint32_t tsfq = tmem + C::tSfQ + 12 * qs;
-        if (hi) {
+        if constexpr (C::kBF) {
+          // bf16 x bf16 -> f32, K = 16 per MMA; 128-byte swizzle atoms of 64 columns, 16 KB apart
+          const uint32_t qb = qaddr + (hi ? 0u : static_cast<uint32_t>(C::kQHiBytes));
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = 32 * (kk & 3) + (C::kBM * 128) * (kk >> 2);
+            const uint64_t ad = ptx::smem_desc(qb + off, 16, 1024, ptx::kSw128);
+            const uint64_t bd = ptx::smem_desc(kaddr + off, 16, 1024, ptx::kSw128);
+            ptx::mma_f16_ss(tS, ad, bd, ptx::idesc_bf16(0, 0, 128, 128), kk > 0);
+          }
+        } else if (hi) {
           constexpr int rb = D;  // fp8 row bytes
           const uint32_t sw = swz_mode(rb);
 #pragma unroll
@@ -417,7 +449,10 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
     const uint32_t bar_id = 1 + quad;           // partner warps (4 + quad, 8 + quad)
     float* red = reinterpret_cast<float*>(smem + C::oRed);
     float* red_l = reinterpret_cast<float*>(smem + C::oRedL);
-    constexpr float kPShift = PVBF16 ? 0.f : 8.f;  // P stored as E4M3(P * 2^8)
+    // MXFP8 PV: lazy rescaling as in attn_pp.cuh (a row keeps its max until a tile raises
+    // it by more than kLazy), P <= 2^kLazy stored as E4M3(P * 2^(8 - kLazy)); bf16 PV: exact max
+    constexpr float kLazy = PVBF16 ? 0.f : 4.f;
+    constexpr float kPShift = PVBF16 ? 0.f : 8.f - kLazy;
     constexpr int kOC = DV / 2;                     // O columns owned by this half
     uint32_t g = 0;                                 // tile ordinal (matches the MMA issuer)
 
@@ -437,7 +472,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
         bool hi;
         plan.entry(e, t, hi);
         if (LOW == kLowHigh) hi = true;
-        const bool two_level = hi || (LOW == kLowNV);
+        const bool two_level = (LOW != kLowBF16) && (hi || (LOW == kLowNV));  // bf16 operands: S_q folded in
         const int k0 = t * C::kBN;
         ptx::mbar_wait(s_full + (g & 1), (g >> 1) & 1);
         ptx::tc_fence_after();
@@ -487,9 +522,11 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
         ptx::named_bar_sync(bar_id, 64);
         mx = fmaxf(mx, rb[(half ^ 1) * 128 + r]);
         const float m_tile = mx * rowf;
-        const float m_new = fmaxf(m_run, m_tile);
+        const float m_cand = fmaxf(m_run, m_tile);
+        const bool upd = PVBF16 ? true : (m_cand > m_run + kLazy);  // always for the first live tile
+        const float m_new = upd ? m_cand : m_run;
         const bool dead = (m_new == -INFINITY);
-        const float alpha = dead ? 1.0f : fast_exp2(m_run - m_new);  // m_run = -inf -> 0
+        const float alpha = (dead || !upd) ? 1.0f : fast_exp2(m_run - m_new);  // m_run = -inf -> 0
         const float bias = dead ? 0.f : (kPShift - m_new);
         const float2 rf2 = make_float2(rowf, rowf), b2 = make_float2(bias, bias);
         float2 ls = make_float2(0.f, 0.f);

@@ -76,6 +76,10 @@ static bool force_single_stream() {
 struct Layout {
   int64_t mq, mk, lq_pad, lk_pad, ch_hi, ch_lo;
   bool low_fp4, pv_bf16, v_convert, tensor_gran, pp;  // pp: ping-pong kernel (permuted, padded K operand)
+  bool deq;        // bf16-operand route (BLOCK granularity or a None format): QK on dequantized bf16 copies
+  bool quant_any;  // deq route needs quantize_dual (not both formats None)
+  // deq route: quantize_dual outputs in the reference layout, per Q (0) / K (1)
+  size_t r_pl[2], r_sl[2], r_hc[2], r_sh[2], r_qs[2];
   // byte offsets
   size_t q_hi, q_lo, k_hi, k_lo, v_codes, v_bf16;  // large buffers
   size_t small_begin, sf_q_hi, sf_q_lo, sf_k_hi, sf_k_lo, sf_v, qs_q, qs_k, ticket, small_end;
@@ -94,21 +98,36 @@ static Layout plan_layout(const DmaAttnArgs* a) {
   L.pv_bf16 = a->pv_mode == DMA_PV_BF16;
   L.v_convert = L.pv_bf16 && a->in_dtype != DMA_DT_BF16;
   L.tensor_gran = a->granularity == DMA_GRAN_TENSOR;
-  L.pp = !L.pv_bf16 && !force_single_stream();
+  L.deq = a->granularity == DMA_GRAN_BLOCK || a->low_format == DMA_FMT_NONE || a->high_format == DMA_FMT_NONE;
+  L.quant_any = !(a->low_format == DMA_FMT_NONE && a->high_format == DMA_FMT_NONE);
+  if (L.deq) L.low_fp4 = true;  // both operand copies exist (bf16)
+  L.pp = !L.pv_bf16 && !force_single_stream() && !L.deq;
   const int64_t k_rows = L.pp ? L.lk_pad : a->len_k;
   const int64_t D = a->head_dim, DV = a->v_dim;
   L.ch_hi = (D / 32 + 3) / 4;
   L.ch_lo = a->low_format == DMA_FMT_NVFP4 ? (D / 16 + 3) / 4 : (D / 32 + 3) / 4;
+  if (L.deq) L.ch_hi = L.ch_lo = 0;  // no scale-factor atoms on the bf16-operand route
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
     off = up256(off + bytes);
     return o;
   };
-  L.q_hi = take(L.mq * a->len_q * D);
-  L.q_lo = L.low_fp4 ? take(L.mq * a->len_q * D / 2) : 0;
-  L.k_hi = take(L.mk * k_rows * D);
-  L.k_lo = L.low_fp4 ? take(L.mk * k_rows * D / 2) : 0;
+  const int64_t obytes_hi = L.deq ? 2 * D : D, obytes_lo = L.deq ? 2 * D : D / 2;  // operand bytes per row
+  L.q_hi = take(L.mq * a->len_q * obytes_hi);
+  L.q_lo = L.low_fp4 ? take(L.mq * a->len_q * obytes_lo) : 0;
+  L.k_hi = take(L.mk * k_rows * obytes_hi);
+  L.k_lo = L.low_fp4 ? take(L.mk * k_rows * obytes_lo) : 0;
+  for (int w = 0; w < 2; ++w) {
+    const int64_t n = (w == 0 ? L.mq * a->len_q : L.mk * a->len_k);  // rows of Q / K
+    const bool on = L.deq && L.quant_any;
+    const int64_t nq = a->granularity == DMA_GRAN_BLOCK ? n * (D / 32) : (a->granularity == DMA_GRAN_TOKEN ? n : (w == 0 ? L.mq : L.mk));
+    L.r_pl[w] = on ? take(n * D / 2) : 0;
+    L.r_sl[w] = on ? take(n * (D / 16)) : 0;
+    L.r_hc[w] = on ? take(n * D) : 0;
+    L.r_sh[w] = on ? take(n * (D / 32)) : 0;
+    L.r_qs[w] = on ? take(nq * 8) : 0;
+  }
   L.v_codes = L.pv_bf16 ? 0 : take(L.mk * L.lk_pad * DV);
   L.v_bf16 = L.v_convert ? take(L.mk * a->len_k * DV * 2) : 0;
   L.small_begin = off;
@@ -154,10 +173,9 @@ int attention_supported(const DmaAttnArgs* a) {
   if (a->tile_m != 128 || a->tile_n != 128) return unsup("sm_100a kernel tiles are 128x128 (tile_m = tile_n = 128)");
   if (a->head_dim != 64 && a->head_dim != 128) return unsup("head_dim must be 64 or 128");
   if (a->v_dim != a->head_dim) return unsup("v_dim must equal head_dim");
-  if (a->high_format != DMA_FMT_MXFP8_E4M3 && a->high_format != DMA_FMT_MXFP8_E5M2)
-    return unsup("high_format must be an MXFP8 format (identity paths are not on the tensor-core kernel)");
-  if (a->low_format == DMA_FMT_NONE) return unsup("low_format=None (identity) is not on the tensor-core kernel");
-  if (a->granularity == DMA_GRAN_BLOCK) return unsup("BLOCK granularity is not on the tensor-core kernel yet");
+  if (a->high_format != DMA_FMT_MXFP8_E4M3 && a->high_format != DMA_FMT_MXFP8_E5M2 && a->high_format != DMA_FMT_NONE)
+    return unsup("high_format must be an MXFP8 format or None");
+  if (a->granularity < 0 || a->granularity > 2) return unsup("unknown granularity");
   if (a->pv_mode != DMA_PV_MXFP8 && a->pv_mode != DMA_PV_BF16) return unsup("bad pv_mode");
   if (a->len_q > (int64_t(1) << 30) || a->len_k > (int64_t(1) << 30)) return unsup("sequence too long");
   return 0;
@@ -173,13 +191,117 @@ __global__ void to_bf16_kernel(const void* src, int dt, int64_t n, __nv_bfloat16
 }
 
 
+// bf16-operand route, phase 1b: the operands the reference's _prepare_operands builds
+// (attention.py:247-279), rounded to bf16: mode 0 = identity (x * c for Q, attention.py:
+// 256-258), 1 = dequantize_high (quantize.py:232-237), 2 = dequantize_low (:215-229),
+// 3 = the low path reuses the high one (8-bit low format, :270-271).
+__global__ void deq_bf16_kernel(int lo_mode, int hi_mode, int nv, int e5, int gran, int64_t n_mat, int64_t rows,
+                                int cols, const uint8_t* pl, const uint8_t* sl, const uint8_t* hc, const uint8_t* sh,
+                                const double* qs, const void* x, int x_dt, int is_query, double c,
+                                __nv_bfloat16* out_hi, __nv_bfloat16* out_lo) {
+  const int64_t n = n_mat * rows * cols;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t rr = i / cols;  // mat * rows + row
+    const int col = static_cast<int>(i % cols);
+    double ident;
+    if (x_dt == DMA_DT_BF16) ident = __bfloat162float(static_cast<const __nv_bfloat16*>(x)[i]);
+    else if (x_dt == DMA_DT_F32) ident = static_cast<const float*>(x)[i];
+    else ident = static_cast<const double*>(x)[i];
+    if (is_query) ident = __dmul_rn(ident, c);
+    double s_q = 1.0;
+    if (hi_mode == 1 || lo_mode == 2 || lo_mode == 3) {
+      if (gran == DMA_GRAN_TOKEN) s_q = qs[rr];
+      else if (gran == DMA_GRAN_BLOCK) s_q = qs[rr * (cols / 32) + col / 32];
+      else s_q = qs[rr / rows];
+    }
+    double hi = ident;
+    if (hi_mode == 1) {
+      const uint32_t cd = hc[i];
+      double e;
+      if (e5) {
+        const uint32_t ex = (cd >> 2) & 0x1F, m = cd & 3;
+        e = ex ? (4.0 + m) * pow2(static_cast<int>(ex) - 17) : m * pow2(-16);
+        if (cd & 0x80) e = -e;
+      } else {
+        e = decode_e4m3(cd);
+      }
+      hi = e * pow2(static_cast<int>(sh[rr * (cols / 32) + col / 32]) - 127) * s_q;
+    }
+    double lo = ident;
+    if (lo_mode == 3) {
+      lo = hi;
+    } else if (lo_mode == 2) {
+      const uint32_t byte = pl[rr * (cols / 2) + col / 2];
+      const uint32_t code = (col & 1) ? (byte >> 4) : (byte & 0xF);
+      const double mags[8] = {0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0};
+      double e = mags[code & 7];
+      if (code & 8) e = -e;
+      lo = nv ? e * decode_e4m3(sl[rr * (cols / 16) + col / 16]) * s_q
+              : e * pow2(static_cast<int>(sl[rr * (cols / 32) + col / 32]) - 127);
+    }
+    out_hi[i] = __float2bfloat16_rn(static_cast<float>(hi));
+    out_lo[i] = __float2bfloat16_rn(static_cast<float>(lo));
+  }
+}
+
+static int quantize_deq(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStream_t st) {
+  const int64_t D = a->head_dim;
+  const bool low_e2m1 = a->low_format == DMA_FMT_NVFP4 || a->low_format == DMA_FMT_MXFP4;
+  const int qlow = low_e2m1 ? a->low_format : DMA_FMT_NVFP4;
+  const int qhigh = a->high_format != DMA_FMT_NONE ? a->high_format : DMA_FMT_MXFP8_E4M3;
+  const int hi_mode = (a->high_format == DMA_FMT_NONE || !L.quant_any) ? 0 : 1;
+  const int lo_mode = (a->low_format == DMA_FMT_NONE || !L.quant_any) ? 0 : (low_e2m1 ? 2 : 3);
+  for (int w = 0; w < 2; ++w) {
+    const bool isq = w == 0;
+    const int64_t rows = isq ? a->len_q : a->len_k, nmat = isq ? L.mq : L.mk;
+    if (rows == 0) continue;
+    if (L.quant_any) {
+      DmaQuantArgs q{};
+      q.x = isq ? a->q : a->k;
+      q.x_dtype = a->in_dtype;
+      q.is_query = isq;
+      q.n_mat = nmat;
+      q.rows = rows;
+      q.cols = D;
+      q.mat_stride = rows * D;
+      q.row_stride = D;
+      q.prescale = a->prescale;
+      q.low_format = qlow;
+      q.high_format = qhigh;
+      q.granularity = a->granularity;
+      q.packed_low = ws + L.r_pl[w];
+      q.scales_low = ws + L.r_sl[w];
+      q.high_codes = ws + L.r_hc[w];
+      q.scales_high = ws + L.r_sh[w];
+      q.quant_scale = reinterpret_cast<double*>(ws + L.r_qs[w]);
+      q.workspace = L.tensor_gran ? ws + (isq ? L.absmax_q : L.absmax_k) : nullptr;
+      q.workspace_bytes = L.tensor_gran ? nmat * 8 : 0;
+      if (int rc = quantize_impl(&q, nullptr, nullptr, nullptr, 0, st, 0)) return rc;
+      g_launches += L.tensor_gran ? 2 : 1;
+    }
+    const int64_t n = nmat * rows * D;
+    int64_t g = (n + 255) / 256;
+    g = g > 148 * 16 ? 148 * 16 : g;
+    deq_bf16_kernel<<<static_cast<unsigned>(g), 256, 0, st>>>(
+        lo_mode, hi_mode, qlow == DMA_FMT_NVFP4, qhigh == DMA_FMT_MXFP8_E5M2, a->granularity, nmat, rows,
+        static_cast<int>(D), ws + L.r_pl[w], ws + L.r_sl[w], ws + L.r_hc[w], ws + L.r_sh[w],
+        reinterpret_cast<const double*>(ws + L.r_qs[w]), isq ? a->q : a->k, a->in_dtype, isq, a->prescale,
+        reinterpret_cast<__nv_bfloat16*>(ws + (isq ? L.q_hi : L.k_hi)),
+        reinterpret_cast<__nv_bfloat16*>(ws + (isq ? L.q_lo : L.k_lo)));
+    DMA_LAUNCH_CHECK();
+    ++g_launches;
+  }
+  return 0;
+}
+
 int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStream_t st) {
   const int64_t D = a->head_dim, DV = a->v_dim;
   const bool nv = a->low_format == DMA_FMT_NVFP4;
   // padded SF atoms / S_q entries must be finite: zero the small region once per call
   DMA_CUDA_TRY(cudaMemsetAsync(ws + L.small_begin, 0, L.small_end - L.small_begin, st));
   ++g_launches;
-  for (int which = 0; which < 2; ++which) {
+  for (int which = 0; which < 2 && !L.deq; ++which) {
     const bool isq = which == 0;
     DmaQuantArgs q{};
     q.x = isq ? a->q : a->k;
@@ -206,6 +328,8 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
     g_launches += L.tensor_gran ? 2 : 1;
   }
   (void)nv;
+  if (L.deq)
+    if (int rc = quantize_deq(a, L, ws, st)) return rc;
   if (a->len_k > 0) {
     if (!L.pv_bf16) {
       // dv in {64, 128} (attention_supported): 256 threads = 256 / (dv/2) key blocks of 32
@@ -276,6 +400,7 @@ static int launch_pp(const AttnParams& p, const PPParams& q, cudaStream_t st) {
 
 template <int D>
 static int dispatch_attn(const AttnParams& p, int low, bool pv_bf16, int64_t items, cudaStream_t st) {
+  if (low == kLowBF16) return pv_bf16 ? launch_attn<D, kLowBF16, true>(p, items, st) : launch_attn<D, kLowBF16, false>(p, items, st);
   if (low == kLowNV) return pv_bf16 ? launch_attn<D, kLowNV, true>(p, items, st) : launch_attn<D, kLowNV, false>(p, items, st);
   if (low == kLowMX4) return pv_bf16 ? launch_attn<D, kLowMX4, true>(p, items, st) : launch_attn<D, kLowMX4, false>(p, items, st);
   return pv_bf16 ? launch_attn<D, kLowHigh, true>(p, items, st) : launch_attn<D, kLowHigh, false>(p, items, st);
@@ -286,12 +411,21 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
   AttnParams p;
   std::memset(&p, 0, sizeof(p));
   const int64_t lq_rows = a->len_q > 0 ? a->len_q : 1, lk_rows = a->len_k > 0 ? a->len_k : 1;
-  if (int rc = make_map(&p.tm_q_hi, ws + L.q_hi, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, lq_rows, L.mq, (int)D)) return rc;
   const int64_t k_rows = L.pp ? L.lk_pad : lk_rows;
+  if (L.deq) {
+    // bf16 operand copies, 64-column (128-byte, 128B-swizzled) boxes
+    const auto bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    if (int rc = make_map(&p.tm_q_hi, ws + L.q_hi, bf, 2, D, lq_rows, L.mq, 64)) return rc;
+    if (int rc = make_map(&p.tm_q_lo, ws + L.q_lo, bf, 2, D, lq_rows, L.mq, 64)) return rc;
+    if (int rc = make_map(&p.tm_k_hi, ws + L.k_hi, bf, 2, D, lk_rows, L.mk, 64)) return rc;
+    if (int rc = make_map(&p.tm_k_lo, ws + L.k_lo, bf, 2, D, lk_rows, L.mk, 64)) return rc;
+  } else {
+  if (int rc = make_map(&p.tm_q_hi, ws + L.q_hi, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, lq_rows, L.mq, (int)D)) return rc;
   if (int rc = make_map(&p.tm_k_hi, ws + L.k_hi, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D, k_rows, L.mk, (int)D)) return rc;
   if (L.low_fp4) {
     if (int rc = make_map(&p.tm_q_lo, ws + L.q_lo, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D / 2, lq_rows, L.mq, (int)D / 2)) return rc;
     if (int rc = make_map(&p.tm_k_lo, ws + L.k_lo, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, D / 2, k_rows, L.mk, (int)D / 2)) return rc;
+  }
   }
   if (L.pv_bf16) {
     const void* vsrc = L.v_convert ? static_cast<const void*>(ws + L.v_bf16) : a->v;
@@ -328,7 +462,8 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
   DMA_CHECK_ARG(items < (int64_t(1) << 31), "too many work items");
   p.n_bh = static_cast<int>(L.mq);
   p.n_items = static_cast<int>(items);
-  const int low = a->low_format == DMA_FMT_NVFP4 ? kLowNV : (a->low_format == DMA_FMT_MXFP4 ? kLowMX4 : kLowHigh);
+  const int low = L.deq ? kLowBF16
+                        : (a->low_format == DMA_FMT_NVFP4 ? kLowNV : (a->low_format == DMA_FMT_MXFP4 ? kLowMX4 : kLowHigh));
   if (L.pp) {
     // ping-pong kernel (block-scaled MXFP8 PV): pairs of heads share one query-tile plan
     PPParams q{};

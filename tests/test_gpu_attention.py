@@ -128,8 +128,6 @@ def test_unsupported_configs_raise():
     q = randn_bf16(1, 256, 64)
     with pytest.raises(d._lib.DmaUnsupported):
         d.mixed_precision_attention(q, q, q, d.AttentionConfig())  # 64-tiles
-    with pytest.raises(d._lib.DmaUnsupported):
-        d.mixed_precision_attention(q, q, q, d.AttentionConfig(tile_m=128, tile_n=128, low_format=None))
     with pytest.raises(ValueError, match="causal"):
         d.mixed_precision_attention(q, q[:128], q[:128], d.AttentionConfig(tile_m=128, tile_n=128))
 
@@ -152,3 +150,49 @@ def test_forward_host_pipeline_matches_device(chunk):
     dev = D().DmaAttention(c)(q.cuda(), k.cuda(), v.cuda())
     assert not host.is_cuda and host.shape == (B, H, N, d)
     assert torch.equal(host, dev.cpu())
+
+
+# bf16-operand route (BLOCK granularity, None formats): QK on bf16 copies of the
+# reference's dequantized operands.  The bf16 rounding (2^-9 relative per operand
+# element) is the only addition to the emulation: ~2.5e-3 rel-L2 with bf16 PV; with
+# MXFP8 PV it also flips some E4M3 roundings of P (~1-1.4e-2 rel-L2 vs the emulation,
+# first B200 run), while the distance to the reference itself stays at the MXFP8-PV level.
+DEQ_CASES = [
+    # name, Lq, Lk, d, low, high, gran, T, S, causal
+    ("block_nvfp4_512_d128", 512, 512, 128, "nvfp4", "e4m3", "block", 128, 128, True),
+    ("block_mxfp4_384_d64", 384, 384, 64, "mxfp4", "e4m3", "block", 128, 0, True),
+    ("block_noncausal_256x512", 256, 512, 128, "nvfp4", "e4m3", "block", 256, 128, False),
+    ("block_low8_256", 256, 256, 128, "mxfp8", "e5m2", "block", 0, 0, True),
+    ("ident_low_512_d128", 512, 512, 128, None, "e4m3", "token", 128, 128, True),
+    ("ident_high_256_d64", 256, 256, 64, "nvfp4", None, "tensor", 128, 0, True),
+    ("ident_both_384", 384, 384, 128, None, None, "token", 0, 0, True),
+]
+TOL_DEQ = {"bf16": (1e-2, 5e-2), "mxfp8": (6e-2, 0.6)}
+TOL_DEQ_EMU = {"bf16": (1e-2, 5e-2), "mxfp8": (3e-2, 0.15)}
+
+
+@pytest.mark.parametrize("pv", ["bf16", "mxfp8"])
+@pytest.mark.parametrize("case", DEQ_CASES, ids=[c[0] for c in DEQ_CASES])
+def test_attention_bf16_operand_route(case, pv):
+    name, lq, lk, d, low, high, gran, T, S, causal = case
+    m = D()
+    lo = {None: (None, None), "nvfp4": (m.NVFP4, O.NVFP4), "mxfp4": (m.MXFP4, O.MXFP4),
+          "mxfp8": (m.MXFP8_E4M3, O.MXFP8_E4M3)}[low]
+    hi = {None: (None, None), "e4m3": (m.MXFP8_E4M3, O.MXFP8_E4M3), "e5m2": (m.MXFP8_E5M2, O.MXFP8_E5M2)}[high]
+    g = {"token": m.Granularity.TOKEN, "block": m.Granularity.BLOCK, "tensor": m.Granularity.TENSOR}[gran]
+    c = m.AttentionConfig(tile_m=128, tile_n=128, diag_window=T, sink_window=S, causal=causal, low_format=lo[0],
+                          high_format=hi[0], granularity=g, pv_mode=pv)
+    oc = O.Cfg(tile_m=128, tile_n=128, diag_window=T, sink_window=S, causal=causal, low_format=lo[1],
+               high_format=hi[1], granularity=gran)
+    seed = zlib.crc32(name.encode()) % 1000
+    q, k, v = randn_bf16(seed, lq, d), randn_bf16(seed + 1, lk, d), randn_bf16(seed + 2, lk, d)
+    got = m.mixed_precision_attention(q, k, v, c)
+    want = O.mixed_precision_attention(q, k, v, oc)
+    emu = O.mixed_precision_attention(q, k, v, oc, pv=pv)
+    rel, mx = errs(got, want)
+    erel, emx = errs(got, emu)
+    print(f"{name} pv={pv}: vs oracle rel_l2={rel:.3e} max_abs={mx:.3e}; vs emulation rel_l2={erel:.3e} "
+          f"max_abs={emx:.3e}")
+    assert np.isfinite(got).all()
+    assert erel <= TOL_DEQ_EMU[pv][0] and emx <= TOL_DEQ_EMU[pv][1], (erel, emx)
+    assert rel <= TOL_DEQ[pv][0] and mx <= TOL_DEQ[pv][1], (rel, mx)
