@@ -112,6 +112,10 @@ int dma_encode_fp8(const double* x, int64_t n, int32_t e5m2, uint8_t* codes, voi
  * Query head h attends with key/value head h / (H / KVH) (GQA).
  * Phase 1 quantizes Q/K (bit-exact quantize_dual) and V into ``workspace``;
  * phase 2 runs the diagonal-tiled attention with tcgen05 block-scaled MMAs.
+ * Covered: tile_m = tile_n = 128, head_dim = v_dim in {64, 128}, TOKEN / TENSOR
+ * granularity with MX formats on the block-scaled QK path; BLOCK granularity and
+ * None (identity) formats on the bf16-operand path (QK on bf16 copies of the
+ * reference's dequantized operands, attention.py:247-279).
  * ------------------------------------------------------------------------- */
 typedef struct {
   const void* q;
