@@ -336,9 +336,12 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
       const int kb_per_cta = 256 / static_cast<int>(DV / 2);
       dim3 grid(static_cast<unsigned>((L.lk_pad / 32 + kb_per_cta - 1) / kb_per_cta), static_cast<unsigned>(L.mk));
       cudaStream_t s = st;
-      if (a->in_dtype == DMA_DT_BF16)
-        quant_v2_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(a->v), a->len_k,
-                                                            static_cast<int>(DV), L.lk_pad, ws + L.v_codes, ws + L.sf_v);
+      if (a->in_dtype == DMA_DT_BF16) {
+        const int kb4 = 256 / static_cast<int>(DV / 4);
+        dim3 grid4(static_cast<unsigned>((L.lk_pad / 32 + kb4 - 1) / kb4), static_cast<unsigned>(L.mk));
+        quant_v4_bf16_kernel<<<grid4, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(a->v), a->len_k,
+                                                   static_cast<int>(DV), L.lk_pad, ws + L.v_codes, ws + L.sf_v);
+      }
       else if (a->in_dtype == DMA_DT_F32)
         quant_v2_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(a->v), a->len_k, static_cast<int>(DV),
                                                     L.lk_pad, ws + L.v_codes, ws + L.sf_v);

@@ -677,4 +677,59 @@ __global__ void __launch_bounds__(256) quant_v2_kernel(const T* __restrict__ v, 
   }
 }
 
+// bf16 V -> MXFP8 along keys, wide variant: a thread owns four adjacent value columns
+// of one 32-key block (8-byte loads, 4-byte code stores; a warp covers 128 contiguous
+// columns of a key row).  Same arithmetic as quant_v2_kernel: the column maxima come
+// from the bf16 bit patterns (integer max), exact like the f32 max it replaces.
+static __global__ void __launch_bounds__(256) quant_v4_bf16_kernel(const __nv_bfloat16* __restrict__ v, int64_t keys, int dv,
+                                                            int64_t keys_pad, uint8_t* __restrict__ codes,
+                                                            uint8_t* __restrict__ sf_op) {
+  const int tpb = dv >> 2;                      // threads per key block
+  const int n = (threadIdx.x % tpb) * 4;        // first of my four columns
+  const int64_t kblk = static_cast<int64_t>(blockIdx.x) * (blockDim.x / tpb) + threadIdx.x / tpb;
+  const int64_t mat = blockIdx.y;
+  if (kblk * 32 >= keys_pad) return;
+  const __nv_bfloat16* src = v + mat * keys * dv + n;
+  uint2 w[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int64_t key = kblk * 32 + i;
+    w[i] = key < keys ? __ldg(reinterpret_cast<const uint2*>(src + key * dv)) : make_uint2(0u, 0u);
+  }
+  uint32_t m01 = 0u, m23 = 0u;  // per-column max |bf16| bit patterns, two columns per word
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    m01 = __vmaxu2(m01, w[i].x & 0x7FFF7FFFu);
+    m23 = __vmaxu2(m23, w[i].y & 0x7FFF7FFFu);
+  }
+  auto expo = [](uint32_t m16) {  // exponent of the column max, as quant_v2_kernel
+    if (m16 == 0u) return -127;
+    const int fl = static_cast<int>((m16 >> 7) & 0xFF) - 127;  // bf16 / f32 subnormals -> -127
+    return min(max(fl - 8, -127), 127);
+  };
+  const int e[4] = {expo(m01 & 0xFFFFu), expo(m01 >> 16), expo(m23 & 0xFFFFu), expo(m23 >> 16)};
+  float inv[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) inv[j] = exp2f(static_cast<float>(-e[j]));
+  uint8_t* dst = codes + mat * keys_pad * dv + n;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float f0 = __uint_as_float(w[i].x << 16), f1 = __uint_as_float(w[i].x & 0xFFFF0000u);
+    const float f2 = __uint_as_float(w[i].y << 16), f3 = __uint_as_float(w[i].y & 0xFFFF0000u);
+    const uint32_t lo = ptx::cvt_e4m3x2(f0 * inv[0], f1 * inv[1]);
+    const uint32_t hi = ptx::cvt_e4m3x2(f2 * inv[2], f3 * inv[3]);
+    *reinterpret_cast<uint32_t*>(dst + (kblk * 32 + i) * dv) = (lo & 0xFFFFu) | (hi << 16);
+  }
+  const int64_t ktile = kblk >> 2;
+  const int64_t ntiles = keys_pad >> 7;
+  const int nchunk = (dv + 127) >> 7;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = n + j;
+    const int64_t off = ((mat * ntiles + ktile) * nchunk + (c >> 7)) * 512 + ((c & 127) & 31) * 16 +
+                        ((c & 127) >> 5) * 4 + (kblk & 3);
+    sf_op[off] = static_cast<uint8_t>(e[j] + 127);
+  }
+}
+
 }  // namespace dma
