@@ -84,6 +84,13 @@ __device__ unsigned int g_trace_n[4];
 // polynomial (exp2_poly2) instead of MUFU.EX2
 constexpr int kPolyPP = DMA_PP_POLY;
 
+#ifndef DMA_PP_HALF_FREE
+#define DMA_PP_HALF_FREE 0
+#endif
+// 1: the S buffer is handed over per 64-column half (s_free[0] / s_free[1]); the next
+// QK is issued as two N = 64 halves, the first overlapping the consumer's second-half load
+constexpr bool kHalfFree = DMA_PP_HALF_FREE != 0;
+
 #ifndef DMA_PP_EARLY_FREE
 #define DMA_PP_EARLY_FREE 0
 #endif
@@ -224,8 +231,8 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
   uint64_t* v_full = k_empty + C::kNK;            // [kNV]
   uint64_t* v_empty = v_full + C::kNV;            // [kNV]
   uint64_t* sq_empty = v_empty + C::kNV;          // [2][kNS]
-  uint64_t* s_free = sq_empty + 2 * C::kNS;       // 1
-  uint64_t* s_full = s_free + 1;                  // [2]
+  uint64_t* s_free = sq_empty + 2 * C::kNS;       // [2] S columns [0,64) / [64,128) copied out
+  uint64_t* s_full = s_free + 2;                  // [2]
   uint64_t* p_full = s_full + 2;                  // [2]
   uint64_t* o_done = p_full + 2;                  // [2]
   uint64_t* sch_full = o_done + 2;                // [kNSch]
@@ -255,7 +262,8 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         ptx::mbar_init(v_empty + i, 1);
       }
       for (int i = 0; i < 2 * C::kNS; ++i) ptx::mbar_init(sq_empty + i, 4 * kSplit);
-      ptx::mbar_init(s_free, 4 * kSplit);
+      ptx::mbar_init(s_free, kHalfFree ? 4 : 4 * kSplit);
+      ptx::mbar_init(s_free + 1, kHalfFree ? 4 : 4 * kSplit);
       for (int i = 0; i < C::kNSch; ++i) {
         ptx::mbar_init(sch_full + i, 1);
         ptx::mbar_init(sch_empty + i, 1 + C::kSoftWarps);
@@ -436,7 +444,8 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         // the single S buffer: wait until its previous user copied it out
         TRACE(true, 2, 26 + x);
         PROF_MARK(0);
-        ptx::mbar_wait(s_free, (su & 1) ^ 1);
+        const uint32_t sfp = (su & 1) ^ 1;
+        ptx::mbar_wait(s_free, sfp);
         PROF_MARK(3);
         TRACE(true, 2, 10 + x);
         ++su;
@@ -469,32 +478,44 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
 #endif
         PROF_MARK(7);
         TRACE(true, 2, 20 + x);
-        const uint32_t kaddr = sbase + C::oK + kslt * C::kKBytes;
-        const uint32_t tsfq = tmem + C::tSfQ(x), tsfk = tmem + C::tSfK(x), tSd = tmem + C::tS;
-        if (hi) {
-          constexpr int rb = D;
-          const uint64_t dh = static_cast<uint64_t>(ptx::desc_hi(8 * rb, swz_mode(rb))) << 32;
+        const uint32_t tsfq = tmem + C::tSfQ(x), tsfk0 = tmem + C::tSfK(x);
+        // one N = 128 QK, or two N = 64 halves (kHalfFree: the second waits for s_free[1]);
+        // the K scale factors of key rows 64h.. are the atom's words 2h, 2h + 1
+        constexpr int kNH = kHalfFree ? 2 : 1, kN = 128 / kNH;
 #pragma unroll
-          for (int kk = 0; kk < D / 32; ++kk) {
-            const uint64_t ad = dh | ptx::desc_lo(sbase + oq + 32 * kk, 16);
-            const uint64_t bd = dh | ptx::desc_lo(kaddr + 32 * kk, 16);
-            const uint32_t id = ptx::idesc_bs(hf, hf, 0, 0, 128, 128, 1, kk & 3, kk & 3);
-            ptx::wu::mma_mxf8f6f4(tSd, ad, bd, id, tsfq + 4 * (kk >> 2), tsfk + 4 * (kk >> 2), kk > 0);
+        for (int hh = 0; hh < kNH; ++hh) {
+          if (hh == 1) {
+            ptx::mbar_wait(s_free + 1, sfp);
+            ptx::tc_fence_after();
           }
-        } else {
-          constexpr int rb = D / 2;
-          const uint64_t dh = static_cast<uint64_t>(ptx::desc_hi(8 * rb, swz_mode(rb))) << 32;
+          const uint32_t tSd = tmem + C::tS + kN * hh, tsfk = tsfk0 + 2 * hh;
+          if (hi) {
+            constexpr int rb = D;
+            const uint32_t kaddr = sbase + C::oK + kslt * C::kKBytes + hh * (kN * rb);
+            const uint64_t dh = static_cast<uint64_t>(ptx::desc_hi(8 * rb, swz_mode(rb))) << 32;
 #pragma unroll
-          for (int kk = 0; kk < D / 64; ++kk) {
-            const uint64_t ad = dh | ptx::desc_lo(sbase + oq + C::kQHiBytes + 32 * kk, 16);
-            const uint64_t bd = dh | ptx::desc_lo(kaddr + 32 * kk, 16);
-            if (LOW == kLowNV) {
-              const uint32_t id = ptx::idesc_bs(1, 1, 0, 0, 128, 128, 0, 0, 0);
-              ptx::wu::mma_nvf4(tSd, ad, bd, id, tsfq + 4 + 4 * kk, tsfk + 4 * kk, kk > 0);
-            } else {
-              const uint32_t sid = (kk & 1) * 2;
-              const uint32_t id = ptx::idesc_bs(1, 1, 0, 0, 128, 128, 1, sid, sid);
-              ptx::wu::mma_mxf4(tSd, ad, bd, id, tsfq + 4 + 4 * (kk >> 1), tsfk + 4 * (kk >> 1), kk > 0);
+            for (int kk = 0; kk < D / 32; ++kk) {
+              const uint64_t ad = dh | ptx::desc_lo(sbase + oq + 32 * kk, 16);
+              const uint64_t bd = dh | ptx::desc_lo(kaddr + 32 * kk, 16);
+              const uint32_t id = ptx::idesc_bs(hf, hf, 0, 0, 128, kN, 1, kk & 3, kk & 3);
+              ptx::wu::mma_mxf8f6f4(tSd, ad, bd, id, tsfq + 4 * (kk >> 2), tsfk + 4 * (kk >> 2), kk > 0);
+            }
+          } else {
+            constexpr int rb = D / 2;
+            const uint32_t kaddr = sbase + C::oK + kslt * C::kKBytes + hh * (kN * rb);
+            const uint64_t dh = static_cast<uint64_t>(ptx::desc_hi(8 * rb, swz_mode(rb))) << 32;
+#pragma unroll
+            for (int kk = 0; kk < D / 64; ++kk) {
+              const uint64_t ad = dh | ptx::desc_lo(sbase + oq + C::kQHiBytes + 32 * kk, 16);
+              const uint64_t bd = dh | ptx::desc_lo(kaddr + 32 * kk, 16);
+              if (LOW == kLowNV) {
+                const uint32_t id = ptx::idesc_bs(1, 1, 0, 0, 128, kN, 0, 0, 0);
+                ptx::wu::mma_nvf4(tSd, ad, bd, id, tsfq + 4 + 4 * kk, tsfk + 4 * kk, kk > 0);
+              } else {
+                const uint32_t sid = (kk & 1) * 2;
+                const uint32_t id = ptx::idesc_bs(1, 1, 0, 0, 128, kN, 1, sid, sid);
+                ptx::wu::mma_mxf4(tSd, ad, bd, id, tsfq + 4 + 4 * (kk >> 1), tsfk + 4 * (kk >> 1), kk > 0);
+              }
             }
           }
         }
@@ -662,7 +683,26 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
             tv[4 * w + 3] = b.y;
           }
         };
-#if DMA_PP_EARLY_FREE
+#if DMA_PP_HALF_FREE
+        if (kSplit == 1) {
+          // first half already landed (waited above): hand S columns [0, 64) back now
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(s_free);
+          scale_words(0);
+          ptx::tmem_ld_wait();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(s_free + 1);
+        } else {
+          scale_words(0);
+          ptx::tmem_ld_wait();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(s_free + hh);  // this warp's column half
+        }
+        TRACE(tw, x, 2);
+#elif DMA_PP_EARLY_FREE
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
         __syncwarp();
