@@ -63,6 +63,7 @@ struct __align__(64) AttnParams {
   int diag_window, sink_window, causal;
   int ch_hi, ch_lo;
   int hfmt;  // high-path element format: 0 = E4M3, 1 = E5M2
+  int tile_m, tile_n;  // plan tile sizes (attention.py:51-80); the kernels' tiles are 128 x 128
 };
 
 template <int D, int DV, int LOW, bool PVBF16>
@@ -214,8 +215,8 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
         item_coords(p, w, bh, qt);
         const int b = bh / p.heads, h = bh % p.heads;
         const int mat_q = bh, mat_k = b * p.kv_heads + h / p.group;
-        Plan plan;
-        plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
+        Plan2 plan;
+        plan.init(qt, p.lq, p.lk, p.tile_m, p.tile_n, p.diag_window, p.sink_window, p.causal != 0);
         if (plan.n == 0) continue;  // nothing to load (the softmax side writes zeros)
         const int qs = ic % C::kNQ;
         ++ic;
@@ -246,7 +247,8 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
         for (int e = 0; e < plan.n; ++e, ++kc, ++vc) {
           int t;
           bool hi;
-          plan.entry(e, t, hi);
+          uint32_t keep;
+          plan.entry(e, qt, t, hi, keep);
           if (LOW == kLowHigh) hi = true;
           const int ks = kc % C::kNK;
           ptx::mbar_wait(k_empty + ks, ((kc / C::kNK) & 1) ^ 1);
@@ -293,15 +295,16 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
       // The tile stream of this CTA, flattened across items.  QK of tile
       // (g + 1) is issued before the PV of tile g (S is double buffered).
       struct Cursor {
-        int w = 0, e = 0, n = 0;
+        int w = 0, e = 0, n = 0, qt = 0;
         uint32_t ic = 0;  // item ordinal in this CTA
-        Plan plan;
+        Plan2 plan;
       };
       auto load_item = [&](Cursor& c) {  // advance c to the first item with a non-empty plan
         while (c.w < p.n_items) {
           int bh, qt;
           item_coords(p, c.w, bh, qt);
-          c.plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
+          c.plan.init(qt, p.lq, p.lk, p.tile_m, p.tile_n, p.diag_window, p.sink_window, p.causal != 0);
+          c.qt = qt;
           c.n = c.plan.n;
           c.e = 0;
           if (c.n > 0) return true;
@@ -330,7 +333,8 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
         }
         int t;
         bool hi;
-        c.plan.entry(c.e, t, hi);
+        uint32_t keep;
+        c.plan.entry(c.e, c.qt, t, hi, keep);
         if (LOW == kLowHigh) hi = true;
         const int ks = kc % C::kNK;
         ptx::mbar_wait(k_full + ks, (kc / C::kNK) & 1);
@@ -461,8 +465,8 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
       item_coords(p, w, bh, qt);
       const int q0 = qt * C::kBM;
       const int qrow = q0 + r;
-      Plan plan;
-      plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
+      Plan2 plan;
+      plan.init(qt, p.lq, p.lk, p.tile_m, p.tile_n, p.diag_window, p.sink_window, p.causal != 0);
       const float sq_q = (qrow < p.lq) ? p.qs_q[static_cast<int64_t>(bh) * p.lq_pad + qrow] : 1.0f;
       float m_run = -INFINITY;
       float2 l2 = make_float2(0.f, 0.f);
@@ -470,7 +474,10 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
       for (int e = 0; e < plan.n; ++e, ++g) {
         int t;
         bool hi;
-        plan.entry(e, t, hi);
+        uint32_t keep;
+        plan.entry(e, qt, t, hi, keep);
+        // quadrant kept by this entry (64-row half a of the tile, 64-column half of this warp)
+        const bool kept = (keep >> (2 * (r >> 6) + half)) & 1u;
         if (LOW == kLowHigh) hi = true;
         const bool two_level = (LOW != kLowBF16) && (hi || (LOW == kLowNV));  // bf16 operands: S_q folded in
         const int k0 = t * C::kBN;
@@ -506,9 +513,9 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
         // causal (attention.py:178-184, applied when k1-1 > q0, :306) and ragged-key masks
         const int kvalid = p.lk - k0;  // keys [k0, k0+kvalid) exist
         const bool need_causal = p.causal && (k0 + (kvalid < C::kBN ? kvalid : C::kBN) - 1 > q0);
-        const bool masked = need_causal || kvalid < C::kBN;
+        const bool masked = need_causal || kvalid < C::kBN || keep != 0xFu;
         if (masked) {
-          const int lim = (need_causal ? min(qrow - k0 + 1, kvalid) : kvalid) - 64 * half;  // keep j < lim
+          const int lim = !kept ? 0 : (need_causal ? min(qrow - k0 + 1, kvalid) : kvalid) - 64 * half;  // keep j < lim
 #pragma unroll
           for (int j = 0; j < 64; ++j)
             if (j >= lim) s[j] = -INFINITY;

@@ -101,7 +101,7 @@ static Layout plan_layout(const DmaAttnArgs* a) {
   L.deq = a->granularity == DMA_GRAN_BLOCK || a->low_format == DMA_FMT_NONE || a->high_format == DMA_FMT_NONE;
   L.quant_any = !(a->low_format == DMA_FMT_NONE && a->high_format == DMA_FMT_NONE);
   if (L.deq) L.low_fp4 = true;  // both operand copies exist (bf16)
-  L.pp = !L.pv_bf16 && !force_single_stream() && !L.deq;
+  L.pp = !L.pv_bf16 && !force_single_stream() && !L.deq && a->tile_m == 128 && a->tile_n == 128;
   const int64_t k_rows = L.pp ? L.lk_pad : a->len_k;
   const int64_t D = a->head_dim, DV = a->v_dim;
   L.ch_hi = (D / 32 + 3) / 4;
@@ -170,7 +170,8 @@ int attention_supported(const DmaAttnArgs* a) {
     set_error("%s", why);
     return DMA_EUNSUPPORTED;
   };
-  if (a->tile_m != 128 || a->tile_n != 128) return unsup("sm_100a kernel tiles are 128x128 (tile_m = tile_n = 128)");
+  if ((a->tile_m != 64 && a->tile_m != 128) || (a->tile_n != 64 && a->tile_n != 128))
+    return unsup("plan tiles must be 64 or 128 (tile_m, tile_n); the sm_100a kernels walk 128 x 128 tiles");
   if (a->head_dim != 64 && a->head_dim != 128) return unsup("head_dim must be 64 or 128");
   if (a->v_dim != a->head_dim) return unsup("v_dim must equal head_dim");
   if (a->high_format != DMA_FMT_MXFP8_E4M3 && a->high_format != DMA_FMT_MXFP8_E5M2 && a->high_format != DMA_FMT_NONE)
@@ -460,6 +461,8 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
   p.ch_hi = static_cast<int>(L.ch_hi);
   p.ch_lo = static_cast<int>(L.ch_lo);
   p.hfmt = a->high_format == DMA_FMT_MXFP8_E5M2 ? 1 : 0;
+  p.tile_m = a->tile_m;
+  p.tile_n = a->tile_n;
   const int64_t items = L.mq * p.n_qt;
   if (items == 0) return 0;
   DMA_CHECK_ARG(items < (int64_t(1) << 31), "too many work items");

@@ -103,6 +103,98 @@ struct Plan {
   }
 };
 
+// Precision / visit status of key tile kj in this plan (the inverse of entry()).
+__host__ __device__ inline void plan_status(const Plan& pl, int32_t kj, bool& visited, bool& high) {
+  if (pl.causal) {
+    visited = kj < pl.n;
+    high = (kj < pl.lo0) || (kj >= pl.lo1);
+  } else {
+    visited = kj < pl.n_tiles;
+    high = (kj < pl.n_sink) || (kj >= pl.w0 && kj < pl.w1);
+  }
+}
+
+// Entries of a 128 x 128 kernel tile walk for a plan with tile_m, tile_n in {64, 128}
+// (attention.py:191-233 at the plan's own tile size): for query tile q128 and key tile
+// kt the 2 x 2 (or 2 x 1, 1 x 2) plan sub-tiles ("quadrants") are classified
+// high / low / unvisited; a key tile gives one entry per precision present, with a
+// 4-bit mask (bit 2a + b) of the quadrants the entry keeps -- the softmax sets the
+// other quadrants to -inf.  tile_m = tile_n = 128 gives exactly Plan's tiles (in key
+// order).  Used by the single-stream kernel; sequential (next()), like every consumer.
+struct Plan2 {
+  Plan pa[2];
+  int32_t ra, rb, nq, n_kt, n;
+  int32_t kt, sub;  // generator state
+  __host__ __device__ void init(int64_t q128, int64_t len_q, int64_t len_k, int32_t tm, int32_t tn, int32_t T,
+                                int32_t S, bool causal) {
+    ra = tm == 64 ? 2 : 1;
+    rb = tn == 64 ? 2 : 1;
+    nq = static_cast<int32_t>(ceil_div(len_q, tm));
+    for (int a = 0; a < ra; ++a) pa[a].init(q128 * ra + a, len_q, len_k, tm, tn, T, S, causal);
+    n_kt = static_cast<int32_t>(ceil_div(len_k, 128));
+    n = 0;
+    for (int32_t t = 0; t < n_kt; ++t) {
+      uint32_t hm, lm;
+      masks(q128, t, hm, lm);
+      n += (hm ? 1 : 0) + (lm ? 1 : 0);
+    }
+    kt = 0;
+    sub = 0;
+  }
+  __host__ __device__ void masks(int64_t q128, int32_t t, uint32_t& hm, uint32_t& lm) const {
+    hm = lm = 0u;
+    for (int a = 0; a < ra; ++a) {
+      if (q128 * ra + a >= nq) continue;  // ragged end: no such query sub-tile
+      for (int b = 0; b < rb; ++b) {
+        bool vis, hi;
+        plan_status(pa[a], t * rb + b, vis, hi);
+        if (!vis) continue;
+        // a 128-row / 128-column plan tile covers both quadrants of its dimension
+        uint32_t bits = 0u;
+        for (int aa = 0; aa < 2; ++aa)
+          for (int bb = 0; bb < 2; ++bb)
+            if ((ra == 2 ? aa == a : true) && (rb == 2 ? bb == b : true)) bits |= 1u << (2 * aa + bb);
+        (hi ? hm : lm) |= bits;
+      }
+    }
+  }
+  // entry e (callers walk e = 0, 1, 2, ... in order): tile_m = tile_n = 128 keeps the
+  // reference's visit order exactly (Plan::entry); otherwise key order.
+  __host__ __device__ void entry(int32_t e, int64_t q128, int32_t& t, bool& high, uint32_t& keep) {
+    if (ra == 1 && rb == 1) {
+      pa[0].entry(e, t, high);
+      keep = 0xFu;
+      return;
+    }
+    next(q128, t, high, keep);
+  }
+  // next entry: key tile t, precision, quadrant keep mask; false when done
+  __host__ __device__ bool next(int64_t q128, int32_t& t, bool& high, uint32_t& keep) {
+    while (kt < n_kt) {
+      uint32_t hm, lm;
+      masks(q128, kt, hm, lm);
+      if (sub == 0) {
+        sub = 1;
+        if (hm) {
+          t = kt;
+          high = true;
+          keep = hm;
+          return true;
+        }
+      }
+      ++kt;
+      sub = 0;
+      if (lm) {
+        t = kt - 1;
+        high = false;
+        keep = lm;
+        return true;
+      }
+    }
+    return false;
+  }
+};
+
 // Key permutation of the ping-pong kernel (attn_pp.cuh): inside a 128-key tile,
 // key k = 32 G + 8 m + r sits in operand row 8 (4 G + r / 2) + 2 m + r % 2, and its
 // S_q^K in slot 36 m + 8 G + r of the tile's 144 (kSqkTile) slots.  (With this order the 16x256b TMEM fragment a

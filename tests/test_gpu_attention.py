@@ -127,7 +127,7 @@ def test_unsupported_configs_raise():
     d = D()
     q = randn_bf16(1, 256, 64)
     with pytest.raises(d._lib.DmaUnsupported):
-        d.mixed_precision_attention(q, q, q, d.AttentionConfig())  # 64-tiles
+        d.mixed_precision_attention(q, q, q, d.AttentionConfig(tile_m=32, tile_n=32))  # 32-tiles
     with pytest.raises(ValueError, match="causal"):
         d.mixed_precision_attention(q, q[:128], q[:128], d.AttentionConfig(tile_m=128, tile_n=128))
 
@@ -196,3 +196,51 @@ def test_attention_bf16_operand_route(case, pv):
     assert np.isfinite(got).all()
     assert erel <= TOL_DEQ_EMU[pv][0] and emx <= TOL_DEQ_EMU[pv][1], (erel, emx)
     assert rel <= TOL_DEQ[pv][0] and mx <= TOL_DEQ[pv][1], (rel, mx)
+
+
+# Plan tiles of 64 (the reference's default AttentionConfig): the single-stream kernel walks
+# 128 x 128 tiles and masks per 64 x 64 quadrant (Plan2): a key tile whose quadrants mix
+# precisions is visited once per precision.  Visit order is key order (not the plan's), so
+# the lazy max decisions of the MXFP8-PV emulation can differ; bf16 PV stays tight.
+TILE_CASES = [
+    # name, Lq, Lk, d, low, tm, tn, T, S, causal
+    ("default_cfg_512_d64", 512, 512, 64, "nvfp4", 64, 64, 0, 0, True),
+    ("t64_w128_s64_640_d128", 640, 640, 128, "nvfp4", 64, 64, 128, 64, True),
+    ("t64x128_w256_384_d128", 384, 384, 128, "mxfp4", 64, 128, 256, 128, True),
+    ("t128x64_w64_320_d64", 320, 320, 64, "nvfp4", 128, 64, 64, 64, True),
+    ("t64_noncausal_200x448", 200, 448, 128, "nvfp4", 64, 64, 128, 64, False),
+]
+TOL_TILE_EMU = {"bf16": (2e-3, 5e-3), "mxfp8": (4e-2, 0.15)}
+
+
+@pytest.mark.parametrize("pv", ["bf16", "mxfp8"])
+@pytest.mark.parametrize("case", TILE_CASES, ids=[c[0] for c in TILE_CASES])
+def test_attention_plan_tiles_64(case, pv):
+    name, lq, lk, d, low, tm, tn, T, S, causal = case
+    m = D()
+    lo = {"nvfp4": (m.NVFP4, O.NVFP4), "mxfp4": (m.MXFP4, O.MXFP4)}[low]
+    c = m.AttentionConfig(tile_m=tm, tile_n=tn, diag_window=T, sink_window=S, causal=causal, low_format=lo[0],
+                          pv_mode=pv)
+    oc = O.Cfg(tile_m=tm, tile_n=tn, diag_window=T, sink_window=S, causal=causal, low_format=lo[1])
+    seed = zlib.crc32(name.encode()) % 1000
+    q, k, v = randn_bf16(seed, lq, d), randn_bf16(seed + 1, lk, d), randn_bf16(seed + 2, lk, d)
+    got = m.mixed_precision_attention(q, k, v, c)
+    want = O.mixed_precision_attention(q, k, v, oc)
+    emu = O.mixed_precision_attention(q, k, v, oc, pv=pv)
+    rel, mx = errs(got, want)
+    erel, emx = errs(got, emu)
+    print(f"{name} pv={pv}: vs oracle rel_l2={rel:.3e} max_abs={mx:.3e}; vs emulation rel_l2={erel:.3e} "
+          f"max_abs={emx:.3e}")
+    assert np.isfinite(got).all()
+    assert erel <= TOL_TILE_EMU[pv][0] and emx <= TOL_TILE_EMU[pv][1], (erel, emx)
+    assert rel <= TOL[pv][0] and mx <= TOL[pv][1], (rel, mx)
+
+
+def test_default_config_runs():
+    """AttentionConfig() (64 x 64 tiles, no windows: the reference default) is a drop-in call."""
+    m = D()
+    q, k, v = randn_bf16(5, 256, 64), randn_bf16(6, 256, 64), randn_bf16(7, 256, 64)
+    got = m.mixed_precision_attention(q, k, v, m.AttentionConfig())
+    want = O.mixed_precision_attention(q, k, v, O.Cfg(tile_m=64, tile_n=64))
+    rel, mx = errs(got, want)
+    assert rel <= TOL["mxfp8"][0] and mx <= TOL["mxfp8"][1], (rel, mx)
