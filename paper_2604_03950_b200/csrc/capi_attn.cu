@@ -173,7 +173,7 @@ int attention_supported(const DmaAttnArgs* a) {
   if ((a->tile_m != 64 && a->tile_m != 128) || (a->tile_n != 64 && a->tile_n != 128))
     return unsup("plan tiles must be 64 or 128 (tile_m, tile_n); the sm_100a kernels walk 128 x 128 tiles");
   if (a->head_dim != 64 && a->head_dim != 128) return unsup("head_dim must be 64 or 128");
-  if (a->v_dim != a->head_dim) return unsup("v_dim must equal head_dim");
+  if (a->v_dim != 64 && a->v_dim != 128) return unsup("v_dim must be 64 or 128");
   if (a->high_format != DMA_FMT_MXFP8_E4M3 && a->high_format != DMA_FMT_MXFP8_E5M2 && a->high_format != DMA_FMT_NONE)
     return unsup("high_format must be an MXFP8 format or None");
   if (a->granularity < 0 || a->granularity > 2) return unsup("unknown granularity");
@@ -375,10 +375,10 @@ static int num_sms() {
   return n;
 }
 
-template <int D, int LOW, bool PVBF16>
+template <int D, int DV, int LOW, bool PVBF16>
 static int launch_attn(const AttnParams& p, int64_t items, cudaStream_t st) {
-  using C = AttnCfg<D, D, LOW, PVBF16>;
-  auto kern = dma_attn_kernel<D, D, LOW, PVBF16>;
+  using C = AttnCfg<D, DV, LOW, PVBF16>;
+  auto kern = dma_attn_kernel<D, DV, LOW, PVBF16>;
   const int smem = C::kSmemBytes > 120 * 1024 ? C::kSmemBytes : 120 * 1024;  // one CTA per SM (TMEM 512 cols)
   DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   // persistent: one CTA per SM, items strided across CTAs (longest first)
@@ -389,10 +389,10 @@ static int launch_attn(const AttnParams& p, int64_t items, cudaStream_t st) {
   return 0;
 }
 
-template <int D, int LOW>
+template <int D, int DV, int LOW>
 static int launch_pp(const AttnParams& p, const PPParams& q, cudaStream_t st) {
-  using C = PPCfg<D, D, LOW>;
-  auto kern = dma_attn_pp_kernel<D, D, LOW>;
+  using C = PPCfg<D, DV, LOW>;
+  auto kern = dma_attn_pp_kernel<D, DV, LOW>;
   static_assert(C::kSmemBytes <= 227 * 1024, "smem budget");
   DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
   const int grid = q.n_pairs < num_sms() ? q.n_pairs : num_sms();
@@ -402,12 +402,19 @@ static int launch_pp(const AttnParams& p, const PPParams& q, cudaStream_t st) {
   return 0;
 }
 
-template <int D>
+template <int D, int DV>
 static int dispatch_attn(const AttnParams& p, int low, bool pv_bf16, int64_t items, cudaStream_t st) {
-  if (low == kLowBF16) return pv_bf16 ? launch_attn<D, kLowBF16, true>(p, items, st) : launch_attn<D, kLowBF16, false>(p, items, st);
-  if (low == kLowNV) return pv_bf16 ? launch_attn<D, kLowNV, true>(p, items, st) : launch_attn<D, kLowNV, false>(p, items, st);
-  if (low == kLowMX4) return pv_bf16 ? launch_attn<D, kLowMX4, true>(p, items, st) : launch_attn<D, kLowMX4, false>(p, items, st);
-  return pv_bf16 ? launch_attn<D, kLowHigh, true>(p, items, st) : launch_attn<D, kLowHigh, false>(p, items, st);
+  if (low == kLowBF16) return pv_bf16 ? launch_attn<D, DV, kLowBF16, true>(p, items, st) : launch_attn<D, DV, kLowBF16, false>(p, items, st);
+  if (low == kLowNV) return pv_bf16 ? launch_attn<D, DV, kLowNV, true>(p, items, st) : launch_attn<D, DV, kLowNV, false>(p, items, st);
+  if (low == kLowMX4) return pv_bf16 ? launch_attn<D, DV, kLowMX4, true>(p, items, st) : launch_attn<D, DV, kLowMX4, false>(p, items, st);
+  return pv_bf16 ? launch_attn<D, DV, kLowHigh, true>(p, items, st) : launch_attn<D, DV, kLowHigh, false>(p, items, st);
+}
+
+template <int D, int DV>
+static int dispatch_pp(const AttnParams& p, const PPParams& q, int low, cudaStream_t st) {
+  if (low == kLowNV) return launch_pp<D, DV, kLowNV>(p, q, st);
+  if (low == kLowMX4) return launch_pp<D, DV, kLowMX4>(p, q, st);
+  return launch_pp<D, DV, kLowHigh>(p, q, st);
 }
 
 int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStream_t st) {
@@ -478,11 +485,12 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
     const double kv_bytes = static_cast<double>(L.mk) * static_cast<double>(L.lk_pad) * (2.6 * static_cast<double>(D));
     q.head_major = kv_bytes > 48.0 * 1024 * 1024;  // K/V exceed ~L2/2: keep all CTAs on the same heads
     q.ticket = reinterpret_cast<unsigned int*>(ws + L.ticket);
-    if (low == kLowNV) return D == 64 ? launch_pp<64, kLowNV>(p, q, st) : launch_pp<128, kLowNV>(p, q, st);
-    if (low == kLowMX4) return D == 64 ? launch_pp<64, kLowMX4>(p, q, st) : launch_pp<128, kLowMX4>(p, q, st);
-    return D == 64 ? launch_pp<64, kLowHigh>(p, q, st) : launch_pp<128, kLowHigh>(p, q, st);
+    if (D == 64) return DV == 64 ? dispatch_pp<64, 64>(p, q, low, st) : dispatch_pp<64, 128>(p, q, low, st);
+    return DV == 64 ? dispatch_pp<128, 64>(p, q, low, st) : dispatch_pp<128, 128>(p, q, low, st);
   }
-  return D == 64 ? dispatch_attn<64>(p, low, L.pv_bf16, items, st) : dispatch_attn<128>(p, low, L.pv_bf16, items, st);
+  if (D == 64)
+    return DV == 64 ? dispatch_attn<64, 64>(p, low, L.pv_bf16, items, st) : dispatch_attn<64, 128>(p, low, L.pv_bf16, items, st);
+  return DV == 64 ? dispatch_attn<128, 64>(p, low, L.pv_bf16, items, st) : dispatch_attn<128, 128>(p, low, L.pv_bf16, items, st);
 }
 
 static uint8_t* ws_base(const DmaAttnArgs* a) {

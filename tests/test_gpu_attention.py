@@ -244,3 +244,21 @@ def test_default_config_runs():
     want = O.mixed_precision_attention(q, k, v, O.Cfg(tile_m=64, tile_n=64))
     rel, mx = errs(got, want)
     assert rel <= TOL["mxfp8"][0] and mx <= TOL["mxfp8"][1], (rel, mx)
+
+
+@pytest.mark.parametrize("pv", ["bf16", "mxfp8"])
+@pytest.mark.parametrize("d,dv,low,causal", [(128, 64, "nvfp4", True), (64, 128, "mxfp4", True),
+                                             (128, 64, "mxfp4", False)])
+def test_attention_value_dim_differs(d, dv, low, causal, pv):
+    """Dv != d (attention.py:109-119 allows it): V / O carry their own width."""
+    c, oc = cfgs(low, "e4m3", "token", 128, 128, causal, pv)
+    lq, lk = 384, 384 if causal else 512
+    q, k, v = randn_bf16(21, lq, d), randn_bf16(22, lk, d), randn_bf16(23, lk, dv)
+    got = D().mixed_precision_attention(q, k, v, c)
+    assert got.shape == (lq, dv)
+    want = O.mixed_precision_attention(q, k, v, oc)
+    emu = O.mixed_precision_attention(q, k, v, oc, pv=pv)
+    rel, mx = errs(got, want)
+    erel, emx = errs(got, emu)
+    assert erel <= TOL_EMU[pv][0] and emx <= TOL_EMU[pv][1], (erel, emx)
+    assert rel <= TOL[pv][0] and mx <= TOL[pv][1], (rel, mx)
