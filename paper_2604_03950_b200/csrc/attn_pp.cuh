@@ -84,6 +84,12 @@ __device__ unsigned int g_trace_n[4];
 // polynomial (exp2_poly2) instead of MUFU.EX2
 constexpr int kPolyPP = DMA_PP_POLY;
 
+#ifndef DMA_PP_SPLIT_PV
+#define DMA_PP_SPLIT_PV 0
+#endif
+// 1: PVs are issued by one warp per stream (kMma + 1 + x); the kMma warp issues only QKs
+constexpr bool kSplitPV = DMA_PP_SPLIT_PV != 0;
+
 #ifndef DMA_PP_HALF_FREE
 #define DMA_PP_HALF_FREE 0
 #endif
@@ -259,14 +265,14 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       }
       for (int i = 0; i < C::kNV; ++i) {
         ptx::mbar_init(v_full + i, 1);
-        ptx::mbar_init(v_empty + i, 1);
+        ptx::mbar_init(v_empty + i, kSplitPV ? 2 : 1);
       }
       for (int i = 0; i < 2 * C::kNS; ++i) ptx::mbar_init(sq_empty + i, 4 * kSplit);
       ptx::mbar_init(s_free, kHalfFree ? 4 : 4 * kSplit);
       ptx::mbar_init(s_free + 1, kHalfFree ? 4 : 4 * kSplit);
       for (int i = 0; i < C::kNSch; ++i) {
         ptx::mbar_init(sch_full + i, 1);
-        ptx::mbar_init(sch_empty + i, 1 + C::kSoftWarps);
+        ptx::mbar_init(sch_empty + i, (kSplitPV ? 3 : 1) + C::kSoftWarps);
       }
       ptx::fence_barrier_init();
       ptx::tma_prefetch_desc(&p.tm_q_hi);
@@ -568,6 +574,12 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         PROF_MARK(9);
       };
 
+      if (kSplitPV) {
+        for (int e = 0; e < plan.n; ++e) {
+          issue_qk(0, e);
+          if (ns == 2) issue_qk(1, e);
+        }
+      } else {
       issue_qk(0, 0);
       if (ns == 2) issue_qk(1, 0);
       for (int e = 0; e < plan.n; ++e) {
@@ -578,9 +590,63 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
           issue_pv(1, e);
         }
       }
+      }
     }
     PROF_MARK(0);
     PROF_FLUSH(10, 10);
+  } else if (kSplitPV && (warp == kMma + 1 || warp == kMma + 2)) {
+    // =========================== PV issuers (kSplitPV): warp kMma + 1 + x issues stream x's PVs ===========================
+    // PV_x(e) depends only on P_x(e) and V, so it must not queue behind QK_x(e + 1), which
+    // waits for the other stream to release the shared S buffer.  V slots follow the
+    // producer's ring order; a slot is released by 2 arrivals (one commit per reading
+    // stream, or two from the only reader).
+    const int x = warp - (kMma + 1);
+    const uint64_t sf_desc_hi = static_cast<uint64_t>(ptx::desc_hi(128, ptx::kSwNone)) << 32;
+    auto sf_desc = [&](uint32_t off) { return sf_desc_hi | ptx::desc_lo(sbase + off, 0); };
+    const uint32_t tsfp = tmem + C::tSfP + 4u * x, tsfv = tmem + C::tSfV(x), tO = tmem + C::tO(x);
+    ptx::wu::tc_cp_sf(tsfp, sf_desc(C::oSfP));
+    uint32_t vc = 0, pvc = 0;
+    for (uint32_t i = 0;; ++i) {
+      const int ss = i % C::kNSch;
+      ptx::mbar_wait(sch_full + ss, (i / C::kNSch) & 1);
+      const int k = sched[ss];
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(sch_empty + ss);
+      if (k < 0) break;
+      int bh0, bh1, qt;
+      pair_coords(p, pp, k, bh0, bh1, qt);
+      Plan plan;
+      plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
+      if (plan.n == 0) continue;
+      const int ns = bh1 >= 0 ? 2 : 1;
+      const bool shared_kv = ns == 2 && mat_k_of(p, bh0) == mat_k_of(p, bh1);
+      const int nk = shared_kv ? 1 : ns;
+      const uint32_t vc0 = vc;
+      vc += nk * plan.n;
+      if (x >= ns) continue;  // odd head count: stream B idles on this pair
+      constexpr int rb = DV;  // fp8 V row bytes (MN-major)
+      const uint64_t dh = static_cast<uint64_t>(ptx::desc_hi(8 * rb, swz_mode(rb))) << 32;
+      for (int e = 0; e < plan.n; ++e) {
+        ptx::mbar_wait(p_full + x, pvc & 1);
+        ++pvc;
+        ptx::tc_fence_after();
+        const uint32_t vpos = vc0 + nk * e + (shared_kv ? 0 : x);
+        const uint32_t vslt = vpos % C::kNV;
+        ptx::mbar_wait(v_full + vslt, (vpos / C::kNV) & 1);
+        ptx::tc_fence_after();
+        ptx::wu::tc_cp_sf(tsfv, sf_desc(C::oSfV + vslt * 512));
+        const uint32_t vaddr = sbase + C::oV + vslt * C::kVBytes;
+#pragma unroll
+        for (int kk = 0; kk < C::kBN / 32; ++kk) {
+          const uint64_t bd = dh | ptx::desc_lo(vaddr + kk * 32 * rb, 16);
+          const uint32_t id = ptx::idesc_bs(0, 0, 0, 1, 128, DV, 1, kk & 3, kk & 3);
+          ptx::wu::mma_mxf8f6f4_ts(tO, tmem + C::tP(x) + 8 * kk, bd, id, tsfp, tsfv, !(e == 0 && kk == 0));
+        }
+        ptx::wu::tc_commit(v_empty + vslt);
+        if (!shared_kv) ptx::wu::tc_commit(v_empty + vslt);
+        ptx::wu::tc_commit(o_done + x);
+      }
+    }
   }
   } else {
     ptx::setmaxnreg_inc<C::kRegSoft>();

@@ -61,6 +61,24 @@ for r in (2, 3):
     for key, vals in sorted(dm.items()):
         if len(vals) > 10:
             print(f"  {names.get(key[0])} -> {names.get(key[1])}: median {np.median(vals):.0f} cyc  (n={len(vals)})")
+
+# cross-role: P full (stream x) -> next "PV_x go" / "PV_x issued" on the MMA issuer
+mma = ev[2]
+for x in (0, 1):
+    pf = [t for (t, a) in ev[x] if a == 6]
+    go = [t for (t, a) in mma if a == 14 + x]
+    iss = [t for (t, a) in mma if a == 16 + x]
+    import bisect
+    d1, d2 = [], []
+    for t in pf[5:-5]:
+        i = bisect.bisect_left(go, t)
+        if i < len(go):
+            d1.append(go[i] - t)
+        j = bisect.bisect_left(iss, t)
+        if j < len(iss):
+            d2.append(iss[j] - t)
+    if d1:
+        print(f"stream {'AB'[x]}: P full -> PV go median {np.median(d1):.0f}, -> PV issued median {np.median(d2):.0f}")
 # window of the interleaved timeline
 merged = sorted([(t, r, a) for r in range(4) for (t, a) in ev[r]])
 mid = len(merged) // 2
