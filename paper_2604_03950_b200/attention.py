@@ -148,31 +148,64 @@ class DmaAttention:
         _lib.check(_lib.lib().dma_attention_fwd(a, _lib.stream_ptr(stream)), "dma_attention")
         return out
 
-    def forward_host(self, q, k, v, out=None, out_dtype=None, chunk_kv_heads=None):
+    def forward_host(self, q, k, v, out=None, out_dtype=None, chunk_kv_heads=None, graph=True):
         """Forward on HOST tensors [B, H, Lq, D] / [B, KVH, Lk, D] (pinned for full speed).
 
         The problem is cut into chunks of whole KV-head groups (GQA groups never
         split); chunk i's host->device copy, chunk i-1's forward and chunk i-2's
         device->host copy run concurrently on three CUDA streams (two device
         buffer sets), so the PCIe transfers -- not the sum of transfers and
-        compute -- bound the end-to-end time.  Returns ``out`` (host).
+        compute -- bound the end-to-end time.  The pipeline (copies, phase-1 and
+        phase-2 launches, cross-stream events) is captured once per (tensors,
+        shapes) into a CUDA graph and replayed: one launch instead of ~15 host
+        calls per chunk (graph=False runs it eagerly).  Returns ``out`` (host).
         """
         import torch
 
         B, H, Lq, D = q.shape
         _, KVH, Lk, _ = k.shape
-        DV = v.shape[-1]
         _check_qkv(q.shape, k.shape, v.shape, self.cfg.causal)
         if H % KVH:
             raise ValueError(f"heads {H} not divisible by kv_heads {KVH}")
-        G = H // KVH
         odt = out_dtype or (torch.bfloat16 if q.dtype == torch.bfloat16 else torch.float32)
         if out is None:
-            out = torch.empty((B, H, Lq, DV), dtype=odt, pin_memory=True)
+            out = torch.empty((B, H, Lq, v.shape[-1]), dtype=odt, pin_memory=True)
         if chunk_kv_heads is None:
             # >= 2 query heads (one head pair x every q tile fills the 148 SMs at N >= 8K) and
             # up to ~16 chunks per batch element (measured best at c2 / c3: 1 / 2 KV heads)
-            chunk_kv_heads = max(1, min(KVH, max(-(-2 // G), KVH // 16)))
+            chunk_kv_heads = max(1, min(KVH, max(-(-2 // (H // KVH)), KVH // 16)))
+        # the graph pays off where the host calls outnumber the GPU work (small chunks, e.g.
+        # c2: 8.9 -> 2.8 ms); with large chunks its copy nodes overlap worse than eager
+        # streams (c3: 16.7 eager vs 18.2 ms graph), so big chunks run eagerly
+        chunk_bytes = chunk_kv_heads * Lk * D * q.element_size() * (H // KVH + 2)
+        if not graph or chunk_bytes > 24 * 2**20:
+            self._host_pipeline(q, k, v, out, chunk_kv_heads)
+            return out
+        key = tuple((t.data_ptr(), tuple(t.shape), t.dtype) for t in (q, k, v, out)) + (chunk_kv_heads,)
+        graphs = self.__dict__.setdefault("_graphs", {})
+        g = graphs.get(key)
+        if g is None:
+            self._host_pipeline(q, k, v, out, chunk_kv_heads)  # eager run: allocations, checks
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._host_pipeline(q, k, v, out, chunk_kv_heads)
+            if len(graphs) >= 4:
+                graphs.pop(next(iter(graphs)))
+            graphs[key] = g
+            torch.cuda.synchronize()
+            return out
+        g.replay()
+        return out
+
+    def _host_pipeline(self, q, k, v, out, chunk_kv_heads):
+        import torch
+
+        B, H, Lq, D = q.shape
+        _, KVH, Lk, _ = k.shape
+        DV = v.shape[-1]
+        G = H // KVH
+        odt = out.dtype
         units = [(b, h0, min(KVH, h0 + chunk_kv_heads)) for b in range(B) for h0 in range(0, KVH, chunk_kv_heads)]
         cur = torch.cuda.current_stream()
         s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
@@ -212,13 +245,11 @@ class DmaAttention:
                 out[b : b + 1, h0 * G : h1 * G].copy_(do, non_blocking=True)
                 ev_out[j] = torch.cuda.Event()
                 ev_out[j].record(s_out)
-            for t in (dq, dk, dv, do):
-                t.record_stream(s_in)
-                t.record_stream(s_cmp)
-                t.record_stream(s_out)
+        for t in [x for bs in bufs for x in bs] + [f._ws for f in fwds]:
+            for st in (s_in, s_cmp, s_out):
+                t.record_stream(st)
         for st in (s_in, s_cmp, s_out):
             cur.wait_stream(st)
-        return out
 
 
 def dma_attention(q, k, v, cfg: AttentionConfig, out=None, out_dtype=None, stream=None):

@@ -145,11 +145,16 @@ def test_forward_host_pipeline_matches_device(chunk):
     k = torch.randn(B, KVH, N, d, generator=g).to(torch.bfloat16).pin_memory()
     v = torch.randn(B, KVH, N, d, generator=g).to(torch.bfloat16).pin_memory()
     fwd = D().DmaAttention(c)
-    host = fwd.forward_host(q, k, v, chunk_kv_heads=chunk)
+    out = torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory()
+    host = fwd.forward_host(q, k, v, out=out, chunk_kv_heads=chunk)  # eager run + CUDA-graph capture
     torch.cuda.synchronize()
     dev = D().DmaAttention(c)(q.cuda(), k.cuda(), v.cuda())
     assert not host.is_cuda and host.shape == (B, H, N, d)
     assert torch.equal(host, dev.cpu())
+    out.zero_()
+    fwd.forward_host(q, k, v, out=out, chunk_kv_heads=chunk)  # graph replay
+    torch.cuda.synchronize()
+    assert torch.equal(out, dev.cpu())
 
 
 # bf16-operand route (BLOCK granularity, None formats): QK on bf16 copies of the
