@@ -132,6 +132,12 @@ struct Plan2 {
     nq = static_cast<int32_t>(ceil_div(len_q, tm));
     for (int a = 0; a < ra; ++a) pa[a].init(q128 * ra + a, len_q, len_k, tm, tn, T, S, causal);
     n_kt = static_cast<int32_t>(ceil_div(len_k, 128));
+    kt = 0;
+    sub = 0;
+    if (ra == 1 && rb == 1) {  // 128 x 128 plan tiles: the plan itself (no quadrant walk)
+      n = pa[0].n;
+      return;
+    }
     n = 0;
     for (int32_t t = 0; t < n_kt; ++t) {
       uint32_t hm, lm;
