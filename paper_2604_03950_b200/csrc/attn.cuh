@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
 
   if (warp == 0) {
     // =========================== TMA producer ===========================
-    if (lane == 0) {
+    {  // whole warp: issue ops elect one lane inside the asm (ptx::wu)
       uint32_t kc = 0, vc = 0, ic = 0;  // ring counters (continue across items)
       for (int w = blockIdx.x; w < p.n_items; w += gridDim.x) {
         int bh, qt;
@@ -225,22 +225,22 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
         if (LOW != kLowHigh) qbytes += C::kQLoBytes + 512 * C::kChLo;
         uint8_t* qdst = smem + C::oQ + qs * C::kQStage;
         uint8_t* sfq = smem + C::oSfQ + qs * C::kSfQStage;
-        ptx::mbar_arrive_expect_tx(q_full + qs, qbytes);
+        ptx::wu::mbar_arrive_expect_tx(q_full + qs, qbytes);
         if constexpr (C::kBF) {
           // bf16 operands: 64-column (128-byte) swizzle boxes, hi then lo
 #pragma unroll
           for (int hb = 0; hb < D / 64; ++hb) {
-            ptx::tma_load_3d(qdst + hb * (C::kBM * 128), &p.tm_q_hi, q_full + qs, hb * 64, qt * C::kBM, mat_q);
-            ptx::tma_load_3d(qdst + C::kQHiBytes + hb * (C::kBM * 128), &p.tm_q_lo, q_full + qs, hb * 64, qt * C::kBM,
+            ptx::wu::tma_load_3d(qdst + hb * (C::kBM * 128), &p.tm_q_hi, q_full + qs, hb * 64, qt * C::kBM, mat_q);
+            ptx::wu::tma_load_3d(qdst + C::kQHiBytes + hb * (C::kBM * 128), &p.tm_q_lo, q_full + qs, hb * 64, qt * C::kBM,
                              mat_q);
           }
         } else {
-        ptx::tma_load_3d(qdst, &p.tm_q_hi, q_full + qs, 0, qt * C::kBM, mat_q);
-        ptx::bulk_load(sfq, p.sf_q_hi + (static_cast<int64_t>(mat_q) * rt_q + qt) * p.ch_hi * 512,
+        ptx::wu::tma_load_3d(qdst, &p.tm_q_hi, q_full + qs, 0, qt * C::kBM, mat_q);
+        ptx::wu::bulk_load(sfq, p.sf_q_hi + (static_cast<int64_t>(mat_q) * rt_q + qt) * p.ch_hi * 512,
                        512 * C::kChHi, q_full + qs);
         if (LOW != kLowHigh) {
-          ptx::tma_load_3d(qdst + C::kQHiBytes, &p.tm_q_lo, q_full + qs, 0, qt * C::kBM, mat_q);
-          ptx::bulk_load(sfq + 512 * C::kChHi, p.sf_q_lo + (static_cast<int64_t>(mat_q) * rt_q + qt) * p.ch_lo * 512,
+          ptx::wu::tma_load_3d(qdst + C::kQHiBytes, &p.tm_q_lo, q_full + qs, 0, qt * C::kBM, mat_q);
+          ptx::wu::bulk_load(sfq + 512 * C::kChHi, p.sf_q_lo + (static_cast<int64_t>(mat_q) * rt_q + qt) * p.ch_lo * 512,
                          512 * C::kChLo, q_full + qs);
         }
         }
@@ -254,34 +254,34 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
           ptx::mbar_wait(k_empty + ks, ((kc / C::kNK) & 1) ^ 1);
           const int ch = hi ? C::kChHi : C::kChLo;
           const uint32_t kb = (hi || C::kBF) ? C::kKBytes : C::kKBytes / 2;
-          ptx::mbar_arrive_expect_tx(k_full + ks, kb + 512 * ch + 512);
+          ptx::wu::mbar_arrive_expect_tx(k_full + ks, kb + 512 * ch + 512);
           if constexpr (C::kBF) {
 #pragma unroll
             for (int hb = 0; hb < D / 64; ++hb)
-              ptx::tma_load_3d(smem + C::oK + ks * C::kKBytes + hb * (C::kBN * 128), hi ? &p.tm_k_hi : &p.tm_k_lo,
+              ptx::wu::tma_load_3d(smem + C::oK + ks * C::kKBytes + hb * (C::kBN * 128), hi ? &p.tm_k_hi : &p.tm_k_lo,
                                k_full + ks, hb * 64, t * C::kBN, mat_k);
           } else {
-          ptx::tma_load_3d(smem + C::oK + ks * C::kKBytes, hi ? &p.tm_k_hi : &p.tm_k_lo, k_full + ks, 0,
+          ptx::wu::tma_load_3d(smem + C::oK + ks * C::kKBytes, hi ? &p.tm_k_hi : &p.tm_k_lo, k_full + ks, 0,
                            t * C::kBN, mat_k);
           const uint8_t* sfsrc = (hi ? p.sf_k_hi : p.sf_k_lo) +
                                  (static_cast<int64_t>(mat_k) * rt_k + t) * (hi ? p.ch_hi : p.ch_lo) * 512;
-          ptx::bulk_load(smem + C::oSfK + ks * 512 * C::kChK, sfsrc, 512 * ch, k_full + ks);
+          ptx::wu::bulk_load(smem + C::oSfK + ks * 512 * C::kChK, sfsrc, 512 * ch, k_full + ks);
           }
-          ptx::bulk_load(smem + C::oSqK + ks * 512, p.qs_k + static_cast<int64_t>(mat_k) * p.lk_pad + t * C::kBN,
+          ptx::wu::bulk_load(smem + C::oSqK + ks * 512, p.qs_k + static_cast<int64_t>(mat_k) * p.lk_pad + t * C::kBN,
                          512, k_full + ks);
 
           const int vs = vc % C::kNV;
           ptx::mbar_wait(v_empty + vs, ((vc / C::kNV) & 1) ^ 1);
           uint8_t* vdst = smem + C::oV + vs * C::kVBytes;
           if (PVBF16) {
-            ptx::mbar_arrive_expect_tx(v_full + vs, C::kVBytes);
+            ptx::wu::mbar_arrive_expect_tx(v_full + vs, C::kVBytes);
 #pragma unroll
             for (int half = 0; half < DV / 64; ++half)
-              ptx::tma_load_3d(vdst + half * (C::kBN * 128), &p.tm_v, v_full + vs, half * 64, t * C::kBN, mat_k);
+              ptx::wu::tma_load_3d(vdst + half * (C::kBN * 128), &p.tm_v, v_full + vs, half * 64, t * C::kBN, mat_k);
           } else {
-            ptx::mbar_arrive_expect_tx(v_full + vs, C::kVBytes + 512);
-            ptx::tma_load_3d(vdst, &p.tm_v, v_full + vs, 0, t * C::kBN, mat_k);
-            ptx::bulk_load(smem + C::oSfV + vs * 512, p.sf_v + (static_cast<int64_t>(mat_k) * rt_k + t) * 512, 512,
+            ptx::wu::mbar_arrive_expect_tx(v_full + vs, C::kVBytes + 512);
+            ptx::wu::tma_load_3d(vdst, &p.tm_v, v_full + vs, 0, t * C::kBN, mat_k);
+            ptx::wu::bulk_load(smem + C::oSfV + vs * 512, p.sf_v + (static_cast<int64_t>(mat_k) * rt_k + t) * 512, 512,
                            v_full + vs);
           }
         }
@@ -289,9 +289,9 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
     }
   } else if (warp == 1) {
     // =========================== MMA issuer ===========================
-    if (lane == 0) {
+    {  // whole warp: issue ops elect one lane inside the asm (ptx::wu)
       if (!PVBF16)
-        ptx::tc_cp_sf(tmem + C::tSfP, ptx::smem_desc(ptx::smem_u32(smem + C::oSfP), 0, 128, ptx::kSwNone));
+        ptx::wu::tc_cp_sf(tmem + C::tSfP, ptx::smem_desc(ptx::smem_u32(smem + C::oSfP), 0, 128, ptx::kSwNone));
       // The tile stream of this CTA, flattened across items.  QK of tile
       // (g + 1) is issued before the PV of tile g (S is double buffered).
       struct Cursor {
@@ -324,11 +324,11 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
           ptx::tc_fence_after();
           const uint8_t* sfq = smem + C::oSfQ + qs * C::kSfQStage;
           for (int j = 0; j < C::kChHi; ++j)
-            ptx::tc_cp_sf(tmem + C::tSfQ + 12 * qs + 4 * j,
+            ptx::wu::tc_cp_sf(tmem + C::tSfQ + 12 * qs + 4 * j,
                           ptx::smem_desc(ptx::smem_u32(sfq + 512 * j), 0, 128, ptx::kSwNone));
           if (LOW != kLowHigh)
             for (int j = 0; j < C::kChLo; ++j)
-              ptx::tc_cp_sf(tmem + C::tSfQ + 12 * qs + 4 + 4 * j,
+              ptx::wu::tc_cp_sf(tmem + C::tSfQ + 12 * qs + 4 + 4 * j,
                             ptx::smem_desc(ptx::smem_u32(sfq + 512 * (C::kChHi + j)), 0, 128, ptx::kSwNone));
         }
         int t;
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
         const uint32_t tsfk = tmem + C::tSfK + 8 * (tile_ord & 1);
         const int ch = hi ? C::kChHi : C::kChLo;
         for (int j = 0; j < ch; ++j)
-          ptx::tc_cp_sf(tsfk + 4 * j, ptx::smem_desc(ptx::smem_u32(smem + C::oSfK + ks * 512 * C::kChK + 512 * j),
+          ptx::wu::tc_cp_sf(tsfk + 4 * j, ptx::smem_desc(ptx::smem_u32(smem + C::oSfK + ks * 512 * C::kChK + 512 * j),
                                                      0, 128, ptx::kSwNone));
         const uint32_t tS = tmem + ((tile_ord & 1) ? C::tS1 : C::tS0);
         const uint32_t kaddr = ptx::smem_u32(smem + C::oK + ks * C::kKBytes);
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
             const uint32_t off = 32 * (kk & 3) + (C::kBM * 128) * (kk >> 2);
             const uint64_t ad = ptx::smem_desc(qb + off, 16, 1024, ptx::kSw128);
             const uint64_t bd = ptx::smem_desc(kaddr + off, 16, 1024, ptx::kSw128);
-            ptx::mma_f16_ss(tS, ad, bd, ptx::idesc_bf16(0, 0, 128, 128), kk > 0);
+            ptx::wu::mma_f16_ss(tS, ad, bd, ptx::idesc_bf16(0, 0, 128, 128), kk > 0);
           }
         } else if (hi) {
           constexpr int rb = D;  // fp8 row bytes
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
             const uint64_t bd = ptx::smem_desc(kaddr + 32 * kk, 16, 8 * rb, sw);
             const uint32_t f = static_cast<uint32_t>(p.hfmt);
             const uint32_t id = ptx::idesc_bs(f, f, 0, 0, 128, 128, 1, kk & 3, kk & 3);
-            ptx::mma_mxf8f6f4(tS, ad, bd, id, tsfq + 4 * (kk >> 2), tsfk + 4 * (kk >> 2), kk > 0);
+            ptx::wu::mma_mxf8f6f4(tS, ad, bd, id, tsfq + 4 * (kk >> 2), tsfk + 4 * (kk >> 2), kk > 0);
           }
         } else {
           const uint32_t qlo = qaddr + C::kQHiBytes;
@@ -379,19 +379,19 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
             const uint64_t bd = ptx::smem_desc(kaddr + 32 * kk, 16, 8 * rb, sw);
             if (LOW == kLowNV) {
               const uint32_t id = ptx::idesc_bs(1, 1, 0, 0, 128, 128, 0, 0, 0);
-              ptx::mma_nvf4(tS, ad, bd, id, tsfq + 4 + 4 * kk, tsfk + 4 * kk, kk > 0);
+              ptx::wu::mma_nvf4(tS, ad, bd, id, tsfq + 4 + 4 * kk, tsfk + 4 * kk, kk > 0);
             } else {
               const uint32_t sid = (kk & 1) * 2;
               const uint32_t id = ptx::idesc_bs(1, 1, 0, 0, 128, 128, 1, sid, sid);
-              ptx::mma_mxf4(tS, ad, bd, id, tsfq + 4 + 4 * (kk >> 1), tsfk + 4 * (kk >> 1), kk > 0);
+              ptx::wu::mma_mxf4(tS, ad, bd, id, tsfq + 4 + 4 * (kk >> 1), tsfk + 4 * (kk >> 1), kk > 0);
             }
           }
         }
-        ptx::tc_commit(k_empty + ks);
-        ptx::tc_commit(s_full + (tile_ord & 1));
+        ptx::wu::tc_commit(k_empty + ks);
+        ptx::wu::tc_commit(s_full + (tile_ord & 1));
         ++kc;
         if (++c.e == c.n) {
-          ptx::tc_commit(q_empty + qs);  // Q smem free once these MMAs complete
+          ptx::wu::tc_commit(q_empty + qs);  // Q smem free once these MMAs complete
           c.w += gridDim.x;
           ++c.ic;
           return load_item(c);
@@ -418,22 +418,22 @@ __global__ void __launch_bounds__(384, 1) dma_attn_kernel(const __grid_constant_
           for (int kk = 0; kk < C::kBN / 16; ++kk) {
             const uint64_t bd = ptx::smem_desc(vaddr + kk * 16 * 128, C::kBN * 128, 1024, ptx::kSw128);
             const uint32_t pa = tP + 64 * (kk >> 2) + 8 * (kk & 3);
-            ptx::mma_f16_ts(tmem + C::tO, pa, bd, ptx::idesc_bf16(0, 1, 128, DV), !(first && kk == 0));
+            ptx::wu::mma_f16_ts(tmem + C::tO, pa, bd, ptx::idesc_bf16(0, 1, 128, DV), !(first && kk == 0));
           }
         } else {
           const uint32_t tsfv = tmem + C::tSfV + 4 * (g & 1);
-          ptx::tc_cp_sf(tsfv, ptx::smem_desc(ptx::smem_u32(smem + C::oSfV + vs * 512), 0, 128, ptx::kSwNone));
+          ptx::wu::tc_cp_sf(tsfv, ptx::smem_desc(ptx::smem_u32(smem + C::oSfV + vs * 512), 0, 128, ptx::kSwNone));
           constexpr int rb = DV;  // fp8 V row bytes (MN-major)
 #pragma unroll
           for (int kk = 0; kk < C::kBN / 32; ++kk) {
             const uint64_t bd = ptx::smem_desc(vaddr + kk * 32 * rb, 16, 8 * rb, swz_mode(rb));
             const uint32_t id = ptx::idesc_bs(0, 0, 0, 1, 128, DV, 1, kk & 3, kk & 3);
             const uint32_t pa = tP + 64 * (kk >> 1) + 8 * (kk & 1);
-            ptx::mma_mxf8f6f4_ts(tmem + C::tO, pa, bd, id, tmem + C::tSfP, tsfv, !(first && kk == 0));
+            ptx::wu::mma_mxf8f6f4_ts(tmem + C::tO, pa, bd, id, tmem + C::tSfP, tsfv, !(first && kk == 0));
           }
         }
-        ptx::tc_commit(v_empty + vs);
-        ptx::tc_commit(o_done);
+        ptx::wu::tc_commit(v_empty + vs);
+        ptx::wu::tc_commit(o_done);
         ++vc;
         ++g;
         if (++cp.e == cp.n) {

@@ -130,7 +130,10 @@ struct Plan2 {
     ra = tm == 64 ? 2 : 1;
     rb = tn == 64 ? 2 : 1;
     nq = static_cast<int32_t>(ceil_div(len_q, tm));
-    for (int a = 0; a < ra; ++a) pa[a].init(q128 * ra + a, len_q, len_k, tm, tn, T, S, causal);
+    // constant indices only (pa[] must stay in registers, not local memory)
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+      if (a < ra) pa[a].init(q128 * ra + a, len_q, len_k, tm, tn, T, S, causal);
     n_kt = static_cast<int32_t>(ceil_div(len_k, 128));
     kt = 0;
     sub = 0;
@@ -149,15 +152,20 @@ struct Plan2 {
   }
   __host__ __device__ void masks(int64_t q128, int32_t t, uint32_t& hm, uint32_t& lm) const {
     hm = lm = 0u;
-    for (int a = 0; a < ra; ++a) {
-      if (q128 * ra + a >= nq) continue;  // ragged end: no such query sub-tile
-      for (int b = 0; b < rb; ++b) {
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      if (a >= ra || q128 * ra + a >= nq) continue;  // ragged end: no such query sub-tile
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        if (b >= rb) continue;
         bool vis, hi;
         plan_status(pa[a], t * rb + b, vis, hi);
         if (!vis) continue;
         // a 128-row / 128-column plan tile covers both quadrants of its dimension
         uint32_t bits = 0u;
+#pragma unroll
         for (int aa = 0; aa < 2; ++aa)
+#pragma unroll
           for (int bb = 0; bb < 2; ++bb)
             if ((ra == 2 ? aa == a : true) && (rb == 2 ? bb == b : true)) bits |= 1u << (2 * aa + bb);
         (hi ? hm : lm) |= bits;

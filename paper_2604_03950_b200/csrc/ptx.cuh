@@ -414,6 +414,17 @@ DMA_WU_MMA(mma_mxf8f6f4_ts, "kind::mxf8f6f4.block_scale.scale_vec::1X", "[%1]", 
 DMA_WU_MMA(mma_nvf4, "kind::mxf4nvf4.block_scale.scale_vec::4X", "%1", "l", uint64_t)
 DMA_WU_MMA(mma_mxf4, "kind::mxf4.block_scale.scale_vec::2X", "%1", "l", uint64_t)
 #undef DMA_WU_MMA
+// bf16 x bf16 -> f32 (kind::f16, no scale factors); A from shared memory or TMEM
+__device__ __forceinline__ void mma_f16_ss(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p, e;\n\t setp.ne.b32 p, %4, 0;\n\t" DMA_WU_ELECT
+               "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+               ::"r"(d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void mma_f16_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p, e;\n\t setp.ne.b32 p, %4, 0;\n\t" DMA_WU_ELECT
+               "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+               ::"r"(d), "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc) : "memory");
+}
 
 // Two chained block-scaled MMAs (K chunks 0 and 1 of one tile) + a commit, from one
 // elected lane in one asm block: the second MMA's smem descriptors are the first's +
