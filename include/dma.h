@@ -16,6 +16,8 @@
  *   dma_attention_workspace_bytes           (sizing helper for the above)
  *   dma_high_precision_fraction <- metrics.py:55 high_precision_fraction(...)
  *   dma_tile_plan       <- attention.py:191 causal_tile_plan / :212 noncausal_tile_plan
+ *   dma_decode_attention    (SURVEY 8 f rank 4: decode over an MX key cache; rows of
+ *                            mixed_precision_attention, attention.py:282, for new tokens)
  *
  * Conventions
  *   - every pointer to tensor data is a DEVICE pointer (cudaMalloc / torch);
@@ -152,6 +154,48 @@ int64_t dma_tile_plan(int64_t q_tile, int64_t len_q, int64_t len_k, int32_t tile
                       int64_t cap);
 double dma_high_precision_fraction(int64_t len_q, int64_t len_k, int32_t tile_m, int32_t tile_n,
                                    int32_t diag_window, int32_t sink_window, int32_t causal);
+
+/* ---------------------------------------------------------------------------
+ * Decode over a quantized key cache.  n_q new query rows per sequence at
+ * absolute positions pos .. pos + n_q - 1; query i sees keys [0, pos + i] and
+ * its output equals row pos + i of dma_attention_fwd / mixed_precision_attention
+ * over the whole sequence (causal, same tile_m / tile_n / windows / formats;
+ * TOKEN granularity, so every cached row is quantized once and never changes).
+ *   q_*  : dma_quantize_dual outputs of the new queries, is_query = 1,
+ *          n_mat = batch * heads, rows = n_q (canonical layouts above)
+ *   k_*  : dma_quantize_dual outputs of the cached keys, is_query = 0,
+ *          [batch * kv_heads, capacity, ...] (rows >= pos + n_q are ignored)
+ *   v    : value cache [batch, kv_heads, capacity, v_dim], bf16
+ *   o    : [batch, heads, n_q, v_dim], out_dtype f32 or bf16
+ * The low_format pointers are unused (may be NULL) when low_format is MXFP8
+ * (the reference then scores every tile with the high operands).
+ * QK uses the block-scaled elements exactly (f32 products / sums), P and V stay
+ * f32 / bf16 (no PV quantization in decode).  head_dim, v_dim in {64, 128}.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  const uint8_t* q_packed_low;
+  const uint8_t* q_scales_low;
+  const uint8_t* q_high_codes;
+  const uint8_t* q_scales_high;
+  const double* q_quant_scale;
+  const uint8_t* k_packed_low;
+  const uint8_t* k_scales_low;
+  const uint8_t* k_high_codes;
+  const uint8_t* k_scales_high;
+  const double* k_quant_scale;
+  const void* v;
+  void* o;
+  int32_t v_dtype, out_dtype;
+  int64_t batch, heads, kv_heads, n_q, capacity, pos, head_dim, v_dim;
+  int32_t tile_m, tile_n, diag_window, sink_window;
+  int32_t low_format, high_format, granularity;
+  int32_t _pad;
+  void* workspace;
+  size_t workspace_bytes;
+} DmaDecodeArgs;
+
+size_t dma_decode_workspace_bytes(const DmaDecodeArgs* a);
+int dma_decode_attention(const DmaDecodeArgs* a, void* stream);
 
 /* self-test of one tcgen05 block-scaled MMA tile (used by the GPU tests) */
 int dma_selftest_mma(int32_t kind, int32_t K, const uint8_t* a, const uint8_t* b, const uint8_t* sfa,

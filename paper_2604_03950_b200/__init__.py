@@ -18,4 +18,5 @@ from .attention import (  # noqa: F401
     noncausal_tile_plan,
 )
 from .metrics import MetricReport, high_precision_fraction, similarity  # noqa: F401
+from .decode import DmaKVCache  # noqa: F401
 from .scores import mixed_precision_scores, reference_attention, reference_scores  # noqa: F401

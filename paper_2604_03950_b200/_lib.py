@@ -142,6 +142,7 @@ EXPORTED_SYMBOLS = (
     "dma_encode_fp8", "dma_attention_workspace_bytes", "dma_attention_supported", "dma_attention_fwd",
     "dma_attention_quantize", "dma_attention_core", "dma_tile_plan", "dma_high_precision_fraction",
     "dma_selftest_mma", "dma_last_error", "dma_abi_version", "dma_last_launch_count",
+    "dma_decode_workspace_bytes", "dma_decode_attention",
 )
 
 
