@@ -30,6 +30,8 @@ static int decode_shape(const DmaDecodeArgs* a, DecodeShape& s) {
   if (a->batch < 1 || a->heads < 1 || a->kv_heads < 1 || a->n_q < 1 || a->pos < 0 || a->capacity < 1)
     return fail(DMA_EINVAL, "decode: batch, heads, kv_heads, n_q, capacity must be >= 1 and pos >= 0");
   if (a->heads % a->kv_heads) return fail(DMA_EINVAL, "decode: heads %% kv_heads != 0");
+  if (a->capacity % 32)
+    return fail(DMA_EINVAL, "decode: capacity (%lld) must be a multiple of 32", (long long)a->capacity);
   if (a->pos + a->n_q > a->capacity)
     return fail(DMA_EINVAL, "decode: pos + n_q (%lld) exceeds the cache capacity (%lld)",
                 (long long)(a->pos + a->n_q), (long long)a->capacity);
@@ -60,9 +62,11 @@ static int decode_shape(const DmaDecodeArgs* a, DecodeShape& s) {
   s.rows_total = a->batch * a->heads * a->n_q;
   const int64_t units = a->batch * a->kv_heads * s.n_rg;
   const int64_t len = a->pos + a->n_q;
-  // about two CTAs per SM in total; a split covers at least 256 keys (multiple of 128)
-  int64_t splits = (2 * 148 + units - 1) / units;
-  const int64_t max_splits = (len + 255) / 256;
+  // about three waves of resident CTAs (shared-memory bound residency): measured faster
+  // than one long wave -- short CTAs keep every SM's warps busy through the tail
+  const int per_sm = dec_ctas_per_sm(s.R, static_cast<int>(a->head_dim), static_cast<int>(a->v_dim), s.low);
+  int64_t splits = (static_cast<int64_t>(3 * per_sm) * 148 + units - 1) / units;
+  const int64_t max_splits = (len + 127) / 128;
   splits = splits < 1 ? 1 : (splits > max_splits ? max_splits : splits);
   int64_t kps = (len + splits - 1) / splits;
   kps = (kps + 127) / 128 * 128;
@@ -80,7 +84,8 @@ static size_t decode_ws(const DmaDecodeArgs* a, const DecodeShape& s) {
 
 template <int R, int D, int DV, int LOW>
 static cudaError_t launch_decode(const DecodeParams& p, int grid, cudaStream_t st) {
-  constexpr int smem = DecSmem<R, D, DV>::kBytes;
+  constexpr int smem = DecSmem<R, D, DV, LOW>::kBytes;
+  static_assert(smem <= 227 * 1024, "decode smem");
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(dma_decode_kernel<R, D, DV, LOW>,

@@ -19,7 +19,10 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace dma {
 
@@ -96,21 +99,114 @@ __device__ __forceinline__ void load_hi32(const uint8_t* row, const uint8_t* sf,
     }
 }
 
+// 32 element values (no block scale) of chunk c as 16 f32 pairs, plus the chunk's block
+// scales (NVFP4: one per 16 elements; MX: one per 32, s1 == s0)
+template <int LOW>
+__device__ __forceinline__ void load_lo32_raw(const uint8_t* row, const uint8_t* sf, int c, float2 (&x)[16],
+                                              float& s0, float& s1) {  // shared-memory rows
+  const uint4 w = *reinterpret_cast<const uint4*>(row + 16 * c);
+  if (LOW == kDecLowNV) {
+    const uint32_t two = *reinterpret_cast<const uint16_t*>(sf + 2 * c);
+    const float2 f = fp8x2_to_f2(two, false);
+    s0 = f.x;
+    s1 = f.y;
+  } else {
+    s0 = s1 = e8m0_to_f(sf[c]);
+  }
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) x[4 * i + b] = e2m1x2_to_f2((ws[i] >> (8 * b)) & 0xFFu);
+}
+template <bool kGlobal>
+__device__ __forceinline__ void load_hi32_raw(const uint8_t* row, const uint8_t* sf, int c, bool e5m2,
+                                              float2 (&x)[16], float& s) {
+  uint4 w0, w1;
+  if (kGlobal) {
+    w0 = __ldg(reinterpret_cast<const uint4*>(row + 32 * c));
+    w1 = __ldg(reinterpret_cast<const uint4*>(row + 32 * c + 16));
+    s = e8m0_to_f(__ldg(sf + c));
+  } else {
+    w0 = *reinterpret_cast<const uint4*>(row + 32 * c);
+    w1 = *reinterpret_cast<const uint4*>(row + 32 * c + 16);
+    s = e8m0_to_f(sf[c]);
+  }
+  const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) x[2 * i + h] = fp8x2_to_f2((ws[i] >> (16 * h)) & 0xFFFFu, e5m2);
+}
+// sum over pairs [i0, i0 + n) of q * x (packed f32x2 FMAs), q from shared memory
+template <int N>
+__device__ __forceinline__ float dot_pairs(const float* q, const float2 (&x)[16], int i0) {
+  const float4* q4 = reinterpret_cast<const float4*>(q);
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int e = 0; e < N / 2; ++e) {
+    const float4 qv = q4[(i0 >> 1) + e];
+    acc = __ffma2_rn(make_float2(qv.x, qv.y), x[i0 + 2 * e], acc);
+    acc = __ffma2_rn(make_float2(qv.z, qv.w), x[i0 + 2 * e + 1], acc);
+  }
+  return acc.x + acc.y;
+}
+
 // shared memory: dequantized query rows (low, high) [R][D] f32, P [4 warps][R][32],
 // warp partials (m, l) [4][R] and O [4][R][DV]
-template <int R, int D, int DV>
+template <int R, int D, int DV, int LOW>
 struct DecSmem {
-  static constexpr int oQlo = 0;
+  // per-warp ring of kStages stages; a stage holds one 32-key group of the cache:
+  // the "A" key rows (packed FP4 low, or FP8 high codes when the low format is 8-bit),
+  // their block scales, S_q and the bf16 value rows, all filled by cp.async.bulk
+  static constexpr int kStages = 2;
+  static constexpr int kA = LOW == kDecLow8 ? 32 * D : 32 * D / 2;
+  static constexpr int kAsf = 32 * (D / (LOW == kDecLowNV ? 16 : 32));
+  static constexpr int sA = 0, sAsf = kA, sSq = sAsf + kAsf, sV = sSq + 32 * 8;
+  static constexpr int kStage = (sV + 32 * DV * 2 + 127) / 128 * 128;
+  static constexpr int oRing = 0;
+  static constexpr int oQlo = oRing + 4 * kStages * kStage;
   static constexpr int oQhi = oQlo + R * D * 4;
   static constexpr int oP = oQhi + R * D * 4;
   static constexpr int oML = oP + 4 * R * 32 * 4;
-  static constexpr int oO = oML + 4 * R * 8;
-  static constexpr int kBytes = oO + 4 * R * DV * 4;
+  static constexpr int oBar = oML + 4 * R * 8;
+  static constexpr int oO = oRing;  // warp partials reuse the rings once every warp is done
+  static_assert(4 * R * DV * 4 <= 4 * kStages * kStage, "partials fit in the rings");
+  static constexpr int kBytes = oBar + 4 * kStages * 8;
 };
 
+// host: resident CTAs per SM of dma_decode_kernel<R, D, DV, LOW> (shared memory bound)
+inline int dec_ctas_per_sm(int R, int D, int DV, int low) {
+  int bytes = 0;
+  auto get = [&](auto tag) { bytes = decltype(tag)::kBytes; };
+  auto by_low = [&](auto r, auto d, auto dv) {
+    constexpr int Rv = decltype(r)::value, Dv = decltype(d)::value, DVv = decltype(dv)::value;
+    if (low == kDecLowNV) get(DecSmem<Rv, Dv, DVv, kDecLowNV>{});
+    else if (low == kDecLowMX4) get(DecSmem<Rv, Dv, DVv, kDecLowMX4>{});
+    else get(DecSmem<Rv, Dv, DVv, kDecLow8>{});
+  };
+  auto by_dims = [&](auto r) {
+    using I64 = std::integral_constant<int, 64>;
+    using I128 = std::integral_constant<int, 128>;
+    if (D == 64 && DV == 64) by_low(r, I64{}, I64{});
+    else if (D == 64) by_low(r, I64{}, I128{});
+    else if (DV == 64) by_low(r, I128{}, I64{});
+    else by_low(r, I128{}, I128{});
+  };
+  switch (R) {
+    case 1: by_dims(std::integral_constant<int, 1>{}); break;
+    case 2: by_dims(std::integral_constant<int, 2>{}); break;
+    case 4: by_dims(std::integral_constant<int, 4>{}); break;
+    case 8: by_dims(std::integral_constant<int, 8>{}); break;
+    default: by_dims(std::integral_constant<int, 16>{}); break;
+  }
+  const int n = (228 * 1024) / (bytes + 1024);  // 228 KB per SM, ~1 KB reserved per CTA
+  return n < 1 ? 1 : (n > 4 ? 4 : n);
+}
+
 template <int R, int D, int DV, int LOW>
-__global__ void __launch_bounds__(128) dma_decode_kernel(const DecodeParams p) {
-  using S = DecSmem<R, D, DV>;
+__global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode_kernel(const DecodeParams p) {
+  using S = DecSmem<R, D, DV, LOW>;
   extern __shared__ __align__(16) uint8_t smem[];
   float* q_lo = reinterpret_cast<float*>(smem + S::oQlo);
   float* q_hi = reinterpret_cast<float*>(smem + S::oQhi);
@@ -183,85 +279,123 @@ __global__ void __launch_bounds__(128) dma_decode_kernel(const DecodeParams p) {
   int64_t k_end = k_begin + p.keys_per_split;
   k_end = k_end < last + 1 ? k_end : last + 1;
 
-  float m[R], l[R], o[R][DV / 32];
+  constexpr int NP = DV / 64;  // value-column pairs per lane
+  float m[R], l[R];
+  float2 o[R][NP];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     m[r] = -INFINITY;
     l[r] = 0.f;
 #pragma unroll
-    for (int c = 0; c < DV / 32; ++c) o[r][c] = 0.f;
+    for (int c = 0; c < NP; ++c) o[r][c] = make_float2(0.f, 0.f);
   }
   float* ps = reinterpret_cast<float*>(smem + S::oP) + warp * R * 32;
   const int64_t krow0 = static_cast<int64_t>(mk) * p.cap;
 
-  for (int64_t g0 = k_begin + 32 * warp; g0 < k_end; g0 += 128) {
-    const int64_t j = g0 + lane;
-    const bool in = j < k_end;
-    const int t = static_cast<int>(g0 / p.tile_n);  // the 32-key group lies in one key tile
-    bool hi[R];
-    bool need_lo = false, need_hi = false;
+  // which operand copies a 32-key group needs (per row: the tile's precision for that row)
+  auto needs = [&](int64_t g, bool& nlo, bool& nhi) {
+    const int t = static_cast<int>(g / p.tile_n);  // a 32-key group lies in one key tile
+    nlo = nhi = false;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      hi[r] = LOW == kDecLow8 || t < sink_t || t >= hs[r];
-      if (qrow[r] >= 0 && g0 <= qpos[r]) (hi[r] ? need_hi : need_lo) = true;
+      const bool h = LOW == kDecLow8 || t < sink_t || t >= hs[r];
+      if (qrow[r] >= 0 && g <= qpos[r]) (h ? nhi : nlo) = true;
     }
+  };
+  // producer side of this warp's ring (lane 0): bulk-load the 32 cache rows of group g
+  // (capacity is a multiple of 32, so whole groups stay inside the cache)
+  uint8_t* ring = smem + S::oRing + warp * S::kStages * S::kStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::oBar) + warp * S::kStages;
+  auto issue = [&](int st, int64_t g) {
+    if (g >= k_end) return;
+    bool nlo, nhi;
+    needs(g, nlo, nhi);
+    const bool ldA = LOW == kDecLow8 || nlo;
+    const int64_t r0 = krow0 + g;
+    uint8_t* dst = ring + st * S::kStage;
+    uint32_t bytes = 32 * 8 + 32 * DV * 2 + (ldA ? S::kA + S::kAsf : 0);
+    ptx::mbar_arrive_expect_tx(full + st, bytes);
+    if (ldA) {
+      if (LOW == kDecLow8) {
+        ptx::bulk_load(dst + S::sA, p.k_hi + r0 * D, S::kA, full + st);
+        ptx::bulk_load(dst + S::sAsf, p.k_hi_sf + r0 * (D / 32), S::kAsf, full + st);
+      } else {
+        ptx::bulk_load(dst + S::sA, p.k_lo + r0 * (D / 2), S::kA, full + st);
+        ptx::bulk_load(dst + S::sAsf, p.k_lo_sf + r0 * (S::kAsf / 32), S::kAsf, full + st);
+      }
+    }
+    ptx::bulk_load(dst + S::sSq, p.k_sq + r0, 32 * 8, full + st);
+    ptx::bulk_load(dst + S::sV, p.v + r0 * DV, 32 * DV * 2, full + st);
+  };
+  if (lane == 0) {
+#pragma unroll
+    for (int st = 0; st < S::kStages; ++st) ptx::mbar_init(full + st, 1);
+    ptx::fence_barrier_init();
+#pragma unroll
+    for (int st = 0; st < S::kStages; ++st) issue(st, k_begin + 32 * warp + 128 * st);
+  }
+  __syncwarp();
+
+  int it = 0;
+  for (int64_t g0 = k_begin + 32 * warp; g0 < k_end; g0 += 128, ++it) {
+    const int st = it % S::kStages;
+    const uint8_t* stage = ring + st * S::kStage;
+    const int64_t j = g0 + lane;
+    const bool in = j < k_end;
+    const int t = static_cast<int>(g0 / p.tile_n);
+    bool hi[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) hi[r] = LOW == kDecLow8 || t < sink_t || t >= hs[r];
+    bool need_lo, need_hi;
+    needs(g0, need_lo, need_hi);
     const int64_t kr = krow0 + (in ? j : k_begin);
+    ptx::mbar_wait(full + st, (it / S::kStages) & 1);
     float s[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) s[r] = 0.f;
     if (need_lo) {
       if constexpr (LOW != kDecLow8) {
-        const uint8_t* row = p.k_lo + kr * (D / 2);
-        const uint8_t* sf = p.k_lo_sf + kr * (D / (LOW == kDecLowNV ? 16 : 32));
+        const uint8_t* row = stage + S::sA + lane * (D / 2);
+        const uint8_t* sf = stage + S::sAsf + lane * (S::kAsf / 32);
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
-          float x[32];
-          load_lo32<LOW>(row, sf, c, x);
+          float2 x[16];
+          float s0, s1;
+          load_lo32_raw<LOW>(row, sf, c, x, s0, s1);
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             if (hi[r]) continue;
-            const float4* q4 = reinterpret_cast<const float4*>(q_lo + r * D + 32 * c);
-            float acc = s[r];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const float4 qv = q4[e];
-              acc = fmaf(qv.x, x[4 * e], acc);
-              acc = fmaf(qv.y, x[4 * e + 1], acc);
-              acc = fmaf(qv.z, x[4 * e + 2], acc);
-              acc = fmaf(qv.w, x[4 * e + 3], acc);
-            }
-            s[r] = acc;
+            const float* q = q_lo + r * D + 32 * c;
+            s[r] = fmaf(dot_pairs<8>(q, x, 0), s0, s[r]);
+            s[r] = fmaf(dot_pairs<8>(q, x, 8), s1, s[r]);
           }
         }
       }
     }
     if (need_hi) {
-      const uint8_t* row = p.k_hi + kr * D;
-      const uint8_t* sf = p.k_hi_sf + kr * (D / 32);
+      // 8-bit low format: the staged rows are the high codes; otherwise the (rare) window /
+      // sink groups read the high copy straight from global memory
+      const bool staged = LOW == kDecLow8;
+      const uint8_t* row = staged ? stage + S::sA + lane * D : p.k_hi + kr * D;
+      const uint8_t* sf = staged ? stage + S::sAsf + lane * (D / 32) : p.k_hi_sf + kr * (D / 32);
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
-        float x[32];
-        load_hi32(row, sf, c, e5, x);
+        float2 x[16];
+        float sc;
+        if (staged)
+          load_hi32_raw<false>(row, sf, c, e5, x, sc);
+        else
+          load_hi32_raw<true>(row, sf, c, e5, x, sc);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (!hi[r]) continue;
-          const float4* q4 = reinterpret_cast<const float4*>(q_hi + r * D + 32 * c);
-          float acc = s[r];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float4 qv = q4[e];
-            acc = fmaf(qv.x, x[4 * e], acc);
-            acc = fmaf(qv.y, x[4 * e + 1], acc);
-            acc = fmaf(qv.z, x[4 * e + 2], acc);
-            acc = fmaf(qv.w, x[4 * e + 3], acc);
-          }
-          s[r] = acc;
+          s[r] = fmaf(dot_pairs<16>(q_hi + r * D + 32 * c, x, 0), sc, s[r]);
         }
       }
     }
     // logits (base 2): S_q of both operands (MXFP4 low is single level: no S_q),
     // causal mask, online softmax per row
-    const float sqk = static_cast<float>(p.k_sq[kr]);
+    const float sqk = static_cast<float>(reinterpret_cast<const double*>(stage + S::sSq)[lane]);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const bool vis = in && qrow[r] >= 0 && j <= qpos[r];
@@ -278,39 +412,67 @@ __global__ void __launch_bounds__(128) dma_decode_kernel(const DecodeParams p) {
         pv = vis ? exp2f(x - mn) : 0.f;
         l[r] = l[r] * alpha + pv;              // lane-partial sum
 #pragma unroll
-        for (int c = 0; c < DV / 32; ++c) o[r][c] *= alpha;
+        for (int c = 0; c < NP; ++c) o[r][c] = __fmul2_rn(o[r][c], make_float2(alpha, alpha));
         m[r] = mn;
       }
       ps[r * 32 + lane] = pv;
     }
     __syncwarp();
-    // PV: lane owns value columns [DV/32 * lane, DV/32 * (lane + 1))
+    // PV: lane owns value columns [DV/32 * lane, DV/32 * (lane + 1)), P of 4 keys per load
     const int nk = static_cast<int>((k_end - g0) < 32 ? (k_end - g0) : 32);
-#pragma unroll 4
-    for (int jj = 0; jj < nk; ++jj) {
-      const __nv_bfloat16* vrow = p.v + (krow0 + g0 + jj) * DV + (DV / 32) * lane;
-      float vv[DV / 32];
-      if constexpr (DV == 128) {
-        const uint2 w = __ldg(reinterpret_cast<const uint2*>(vrow));
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.x));
-        const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.y));
-        vv[0] = a.x; vv[1] = a.y; vv[2] = c.x; vv[3] = c.y;
+    const __nv_bfloat16* vst = reinterpret_cast<const __nv_bfloat16*>(stage + S::sV);
+    auto pv_key = [&](int jj, const float* pr) {
+      const __nv_bfloat16* vrow = vst + jj * DV + (DV / 32) * lane;
+      float2 vv[NP];
+      if constexpr (NP == 2) {
+        const uint2 w = *reinterpret_cast<const uint2*>(vrow);
+        vv[0] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.x));
+        vv[1] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.y));
       } else {
-        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(vrow));
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
-        vv[0] = a.x; vv[1] = a.y;
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(vrow);
+        vv[0] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w));
       }
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const float pr = ps[r * 32 + jj];
+      for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int c = 0; c < DV / 32; ++c) o[r][c] = fmaf(pr, vv[c], o[r][c]);
-      }
+        for (int c = 0; c < NP; ++c) o[r][c] = __ffma2_rn(make_float2(pr[r], pr[r]), vv[c], o[r][c]);
+    };
+    int jj = 0;
+#pragma unroll 2
+    for (; jj + 4 <= nk; jj += 4) {
+      float4 p4[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) p4[r] = *reinterpret_cast<const float4*>(ps + r * 32 + jj);
+      float pr[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) pr[r] = p4[r].x;
+      pv_key(jj, pr);
+#pragma unroll
+      for (int r = 0; r < R; ++r) pr[r] = p4[r].y;
+      pv_key(jj + 1, pr);
+#pragma unroll
+      for (int r = 0; r < R; ++r) pr[r] = p4[r].z;
+      pv_key(jj + 2, pr);
+#pragma unroll
+      for (int r = 0; r < R; ++r) pr[r] = p4[r].w;
+      pv_key(jj + 3, pr);
+    }
+    for (; jj < nk; ++jj) {
+      float pr[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) pr[r] = ps[r * 32 + jj];
+      pv_key(jj, pr);
     }
     __syncwarp();
+    // the stage is consumed: refill it with this warp's group kStages ahead
+    if (lane == 0) {
+      ptx::fence_proxy_async_smem();
+      issue(st, g0 + 128 * S::kStages);
+    }
   }
 
-  // warp partials -> shared memory, merged per row by all 128 threads
+  // warp partials -> shared memory (over the rings: wait for every warp), merged per row
+  __syncthreads();
   float2* ml = reinterpret_cast<float2*>(smem + S::oML);
   float* ow = reinterpret_cast<float*>(smem + S::oO);
 #pragma unroll
@@ -320,7 +482,8 @@ __global__ void __launch_bounds__(128) dma_decode_kernel(const DecodeParams p) {
     for (int off = 16; off; off >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
     if (lane == 0) ml[warp * R + r] = make_float2(m[r], ls);
 #pragma unroll
-    for (int c = 0; c < DV / 32; ++c) ow[(warp * R + r) * DV + (DV / 32) * lane + c] = o[r][c];
+    for (int c = 0; c < NP; ++c)
+      reinterpret_cast<float2*>(ow)[((warp * R + r) * DV + (DV / 32) * lane) / 2 + c] = o[r][c];
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < R * DV; idx += blockDim.x) {

@@ -147,6 +147,14 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                ::"r"(smem_u32(bar)) : "memory");
 }
 
+// L2 prefetch of a contiguous global range (16-byte aligned address, size a multiple of 16)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
+  // [gsrc, gsrc + bytes) shrunk to 16-byte boundaries (never touches bytes outside the range)
+  const uint64_t a = (reinterpret_cast<uint64_t>(gsrc) + 15) & ~15ull;
+  const uint64_t e = (reinterpret_cast<uint64_t>(gsrc) + bytes) & ~15ull;
+  if (e > a)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(static_cast<uint32_t>(e - a)) : "memory");
+}
 // smem -> TMEM copy of one 512-byte scale-factor atom (32 rows x 16 B, broadcast to 4 lane quadrants)
 __device__ __forceinline__ void tc_cp_sf(uint32_t taddr, uint64_t sdesc) {
   asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");

@@ -87,8 +87,10 @@ class DmaKVCache:
         # "score with the high operands" (attention.py:269-276), the low copy is unused
         self._qlow = cfg.low_format if cfg.low_format.element.bits == 4 else NVFP4
         self._qhigh = cfg.high_format or MXFP8_E4M3
-        self.keys = _Rows(batch * kv_heads, capacity, head_dim, self._qlow.block_size, device)
-        self.values = torch.zeros((batch, kv_heads, capacity, self.v_dim), dtype=torch.bfloat16, device=device)
+        # rows are allocated in whole 32-key groups (the kernel bulk-loads full groups)
+        self._rows = -(-capacity // 32) * 32
+        self.keys = _Rows(batch * kv_heads, self._rows, head_dim, self._qlow.block_size, device)
+        self.values = torch.zeros((batch, kv_heads, self._rows, self.v_dim), dtype=torch.bfloat16, device=device)
         self._flag = torch.zeros(1, dtype=torch.int32, device=device)
         self._ws = torch.empty(256, dtype=torch.uint8, device=device)   # decode partials
         self._qws = torch.empty(256, dtype=torch.uint8, device=device)  # quantize (unused for TOKEN)
@@ -173,7 +175,7 @@ class DmaKVCache:
         a.v_dtype = _lib.DT_BF16
         a.out_dtype = _lib.DT_BF16 if out.dtype == torch.bfloat16 else _lib.DT_F32
         a.batch, a.heads, a.kv_heads, a.n_q = B, H, KVH, nq
-        a.capacity, a.pos, a.head_dim, a.v_dim = self.capacity, self.length - nq, self.head_dim, self.v_dim
+        a.capacity, a.pos, a.head_dim, a.v_dim = self._rows, self.length - nq, self.head_dim, self.v_dim
         a.tile_m, a.tile_n, a.diag_window, a.sink_window = cfg.tile_m, cfg.tile_n, cfg.diag_window, cfg.sink_window
         a.low_format, a.high_format = format_code(cfg.low_format), format_code(cfg.high_format)
         a.granularity = _lib.GRAN_TOKEN
