@@ -503,6 +503,29 @@ using namespace dma;
 
 extern "C" {
 
+// Empty problems (attention.py:282-310 on zero-length inputs): no query rows -> nothing
+// to write; no keys (non-causal) -> every row has l = 0 and normalises to 0.
+// Returns 1 when the call was handled here.
+static int empty_problem(const DmaAttnArgs* a, cudaStream_t st, int* rc) {
+  if (a->len_q > 0 && a->len_k > 0) return 0;
+  *rc = DMA_OK;
+  if (a->len_q > 0) {
+    if (!a->o) {
+      set_error("null output");
+      *rc = DMA_EINVAL;
+      return 1;
+    }
+    const size_t n = static_cast<size_t>(a->batch * a->heads * a->len_q * a->v_dim) *
+                     (a->out_dtype == DMA_DT_BF16 ? 2 : 4);
+    const cudaError_t e = cudaMemsetAsync(a->o, 0, n, st);
+    if (e != cudaSuccess) {
+      set_error("cudaMemsetAsync: %s", cudaGetErrorString(e));
+      *rc = static_cast<int>(e);
+    }
+  }
+  return 1;
+}
+
 size_t dma_attention_workspace_bytes(const DmaAttnArgs* a) {
   if (validate(a)) return 0;
   return plan_layout(a).total;
@@ -513,6 +536,7 @@ int dma_attention_supported(const DmaAttnArgs* a) { return attention_supported(a
 int dma_attention_quantize(const DmaAttnArgs* a, void* stream) {
   g_launches = 0;
   if (int rc = attention_supported(a)) return rc;
+  if (a->len_q == 0 || a->len_k == 0) return DMA_OK;  // nothing to quantize
   Layout L = plan_layout(a);
   DMA_CHECK_ARG(a->workspace && a->workspace_bytes >= L.total, "workspace too small (%zu < %zu)",
                 a->workspace_bytes, L.total);
@@ -521,6 +545,7 @@ int dma_attention_quantize(const DmaAttnArgs* a, void* stream) {
 
 int dma_attention_core(const DmaAttnArgs* a, void* stream) {
   if (int rc = attention_supported(a)) return rc;
+  if (int rc; empty_problem(a, static_cast<cudaStream_t>(stream), &rc)) return rc;
   Layout L = plan_layout(a);
   DMA_CHECK_ARG(a->workspace && a->workspace_bytes >= L.total, "workspace too small (%zu < %zu)",
                 a->workspace_bytes, L.total);
@@ -531,6 +556,7 @@ int dma_attention_core(const DmaAttnArgs* a, void* stream) {
 int dma_attention_fwd(const DmaAttnArgs* a, void* stream) {
   g_launches = 0;
   if (int rc = attention_supported(a)) return rc;
+  if (int rc; empty_problem(a, static_cast<cudaStream_t>(stream), &rc)) return rc;
   Layout L = plan_layout(a);
   DMA_CHECK_ARG(a->workspace && a->workspace_bytes >= L.total, "workspace too small (%zu < %zu)",
                 a->workspace_bytes, L.total);

@@ -267,3 +267,28 @@ def test_attention_value_dim_differs(d, dv, low, causal, pv):
     erel, emx = errs(got, emu)
     assert erel <= TOL_EMU[pv][0] and emx <= TOL_EMU[pv][1], (erel, emx)
     assert rel <= TOL[pv][0] and mx <= TOL[pv][1], (rel, mx)
+
+
+def test_empty_inputs_match_reference():
+    """attention.py:282-310 on zero-length inputs: no query rows -> an empty result; no keys
+    (non-causal) -> every row normalises an l = 0 sum to 0 (checked against the reference)."""
+    import torch
+
+    import paper_2604_03950_b200 as m
+
+    cfg = m.AttentionConfig(tile_m=128, tile_n=128, diag_window=128, sink_window=128)
+    z = np.zeros((0, 64))
+    out = m.mixed_precision_attention(z, z, z, cfg)
+    assert out.shape == (0, 64) and out.dtype == np.float64
+    nc = m.AttentionConfig(tile_m=128, tile_n=128, diag_window=128, sink_window=128, causal=False)
+    out = m.mixed_precision_attention(np.ones((5, 64)), z, z, nc)
+    assert out.shape == (5, 64) and not out.any()
+    ref = O.mixed_precision_attention(np.ones((5, 64)), z, z, O.Cfg(tile_m=128, tile_n=128, diag_window=128,
+                                                                     sink_window=128, causal=False))
+    assert np.array_equal(out, ref)
+    q = torch.zeros(2, 4, 0, 128, dtype=torch.bfloat16, device="cuda")
+    o = m.DmaAttention(cfg)(q, q[:, :2], q[:, :2])
+    assert o.shape == (2, 4, 0, 128)
+    q = torch.randn(1, 2, 7, 128, device="cuda")
+    o = m.DmaAttention(nc)(q, q[:, :, :0], q[:, :, :0])
+    assert o.shape == (1, 2, 7, 128) and not o.any()
