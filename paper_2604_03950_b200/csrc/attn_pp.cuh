@@ -84,6 +84,9 @@ __device__ unsigned int g_trace_n[4];
 // polynomial (exp2_poly2) instead of MUFU.EX2
 constexpr int kPolyPP = DMA_PP_POLY;
 
+#ifndef DMA_PP_LATE_PV_WAIT
+#define DMA_PP_LATE_PV_WAIT 0
+#endif
 #ifndef DMA_PP_SPLIT_PV
 #define DMA_PP_SPLIT_PV 0
 #endif
@@ -822,11 +825,14 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         m_run = m_new;
         TRACE(tw, x, 3);
         PROF_MARK(3);
-        // P_x (and O_x) are read by PV(e-1): wait for it before overwriting
+        // P_x (and O_x) are read by PV(e-1): wait for it before overwriting.  Late wait:
+        // just before the first P store, so the exps of key group 0 hide the wait
+#if !DMA_PP_LATE_PV_WAIT
         if (e > 0) {
           ptx::mbar_wait(o_done + x, (g - 1) & 1);
           ptx::tc_fence_after();
         }
+#endif
         PROF_MARK(4);
         // exp phases of the two streams alternate when kTurns (named barriers 1 = "A may
         // exp", 2 = "B may exp"): MUFU.EX2 is the shared bottleneck
@@ -871,6 +877,12 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
               ls = (q4 == 1 && j == 0) ? e2 : __fadd2_rn(ls, e2);
             }
           }
+#if DMA_PP_LATE_PV_WAIT
+          if (q4 == 1 && e > 0) {
+            ptx::mbar_wait(o_done + x, (g - 1) & 1);
+            ptx::tc_fence_after();
+          }
+#endif
           if (q4 > 0) ptx::tmem_st8(tmem + C::tP(x) + lane_base + NW * hh + 8 * (q4 - 1), pk);
         }
         if (kTurns && pair2) ptx::named_bar_arrive(2 - x, 256 * kSplit);
