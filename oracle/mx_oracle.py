@@ -466,14 +466,15 @@ def _quantize_p(p: np.ndarray, pv: str) -> np.ndarray:
     return p
 
 
-def mixed_precision_attention(q, k, v, cfg: Cfg, pv: str = "f64") -> np.ndarray:
+def mixed_precision_attention(q, k, v, cfg: Cfg, pv: str = "f64", q_tiles=None) -> np.ndarray:
     """Tile loop + base-2 online softmax (attention.py:150-175, 178-184, 282-310).
 
     ``pv="f64"`` is the reference exactly.  ``pv="mxfp8"`` / ``"bf16"`` add the
     sm_100a kernel's stated PV quantization (P -> E4M3 x 2^4 with V -> MXFP8
     along keys and lazy max rescaling, or P and V in bf16) on top of the same
     algorithm; the row sum l still uses the unquantized P, as the kernel does.
-    Test infrastructure only.
+    ``q_tiles`` (optional): compute only these query tiles (rows of other tiles are NaN),
+    for sampled checks at full sequence lengths.  Test infrastructure only.
     """
     lazy = LAZY_RESCALE.get(pv, 0.0)
     ql, qh, kl, kh, v = operands(q, k, v, cfg)
@@ -483,8 +484,8 @@ def mixed_precision_attention(q, k, v, cfg: Cfg, pv: str = "f64") -> np.ndarray:
         v = _quantize_p(v, "bf16")
     lq, lk = ql.shape[0], kl.shape[0]
     tm, tn = cfg.tile_m, cfg.tile_n
-    out = np.empty((lq, v.shape[1]))
-    for qt in range(_cdiv(lq, tm)):
+    out = np.full((lq, v.shape[1]), np.nan)
+    for qt in (range(_cdiv(lq, tm)) if q_tiles is None else q_tiles):
         q0, q1 = qt * tm, min(qt * tm + tm, lq)
         m = np.full(q1 - q0, -np.inf)
         l = np.zeros(q1 - q0)  # l0 = 0, attention.py:100

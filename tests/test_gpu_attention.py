@@ -292,3 +292,24 @@ def test_empty_inputs_match_reference():
     q = torch.randn(1, 2, 7, 128, device="cuda")
     o = m.DmaAttention(nc)(q, q[:, :, :0], q[:, :, :0])
     assert o.shape == (1, 2, 7, 128) and not o.any()
+
+
+@pytest.mark.parametrize("pv", ["mxfp8", "bf16"])
+def test_full_length_c3_sampled_tiles(pv):
+    """BASELINE c3 sequence length (N = 32768, d = 128, NVFP4 + MXFP8, T = S = 128) on 2 heads:
+    sampled query tiles (first, sink neighbourhood, middle, last) against the oracle run on the
+    same full-length K / V -- the plan, masks and quantization at full size."""
+    import torch
+
+    N, d, H = 32768, 128, 2
+    c, oc = cfgs("nvfp4", "e4m3", "token", 128, 128, True, pv)
+    q, k, v = (randn_bf16(40 + i, H, N, d) for i in range(3))
+    got = D().DmaAttention(c)(*(torch.from_numpy(x)[None].cuda() for x in (q, k, v)),
+                              out_dtype=torch.float32)[0].double().cpu().numpy()
+    tiles = [0, 1, 97, 255]
+    for h in range(H):
+        want = O.mixed_precision_attention(q[h], k[h], v[h], oc, pv=pv, q_tiles=tiles)
+        for t in tiles:
+            r = slice(128 * t, 128 * t + 128)
+            rel, mx = errs(got[h, r], want[r])
+            assert rel <= TOL_EMU[pv][0] and mx <= TOL_EMU[pv][1], (pv, h, t, rel, mx)
