@@ -41,6 +41,20 @@ def d2h():
     ho.copy_(q, non_blocking=True)
 
 
-for name, fn in [("h2d 805MB", h2d), ("d2h 268MB", d2h), ("forward_host", lambda: fwd(hq, hk, hv, out=ho)),
+s2 = torch.cuda.Stream()
+
+
+def both():
+    s2.wait_stream(s)
+    with torch.cuda.stream(s2):
+        ho.copy_(q, non_blocking=True)
+    h2d()
+    s.wait_stream(s2)
+
+
+for chunk in (1, 2, 4):
+    print("forward_host chunk", chunk, timed(lambda: fwd.forward_host(hq, hk, hv, out=ho, chunk_kv_heads=chunk), 7),
+          flush=True)
+for name, fn in [("h2d 805MB + concurrent d2h 268MB", both), ("h2d 805MB", h2d), ("d2h 268MB", d2h), ("forward_host", lambda: fwd(hq, hk, hv, out=ho)),
                  ("h2d 805MB again", h2d), ("forward_host again", lambda: fwd(hq, hk, hv, out=ho))]:
     print(name, timed(fn, 15), flush=True)
