@@ -142,14 +142,16 @@ __device__ __forceinline__ void load_hi32_raw(const uint8_t* row, const uint8_t*
 template <int N>
 __device__ __forceinline__ float dot_pairs(const float* q, const float2 (&x)[16], int i0) {
   const float4* q4 = reinterpret_cast<const float4*>(q);
-  float2 acc = make_float2(0.f, 0.f);
+  float4 qv[N / 2];  // all loads first (independent), then two FFMA2 chains
+#pragma unroll
+  for (int e = 0; e < N / 2; ++e) qv[e] = q4[(i0 >> 1) + e];
+  float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
 #pragma unroll
   for (int e = 0; e < N / 2; ++e) {
-    const float4 qv = q4[(i0 >> 1) + e];
-    acc = __ffma2_rn(make_float2(qv.x, qv.y), x[i0 + 2 * e], acc);
-    acc = __ffma2_rn(make_float2(qv.z, qv.w), x[i0 + 2 * e + 1], acc);
+    a0 = __ffma2_rn(make_float2(qv[e].x, qv[e].y), x[i0 + 2 * e], a0);
+    a1 = __ffma2_rn(make_float2(qv[e].z, qv[e].w), x[i0 + 2 * e + 1], a1);
   }
-  return acc.x + acc.y;
+  return (a0.x + a1.x) + (a0.y + a1.y);
 }
 
 // shared memory: dequantized query rows (low, high) [R][D] f32, P [4 warps][R][32],
