@@ -57,7 +57,9 @@ static int decode_shape(const DmaDecodeArgs* a, DecodeShape& s) {
   const int64_t rows = static_cast<int64_t>(s.group) * a->n_q;
   if (rows > (1 << 20)) return fail(DMA_EUNSUPPORTED, "decode: too many query rows per KV head");
   s.rows_per_kvh = static_cast<int32_t>(rows);
-  s.R = pow2_at_least(static_cast<int>(rows < 16 ? rows : 16));
+  // R <= 8 query rows per CTA: more rows per KV head become more row groups (each streams
+  // the cache again) -- measured faster than R = 16 (register-bound, spills)
+  s.R = pow2_at_least(static_cast<int>(rows < 8 ? rows : 8));
   s.n_rg = static_cast<int32_t>((rows + s.R - 1) / s.R);
   s.rows_total = a->batch * a->heads * a->n_q;
   const int64_t units = a->batch * a->kv_heads * s.n_rg;
@@ -103,8 +105,7 @@ static cudaError_t dispatch_r(int R, const DecodeParams& p, int grid, cudaStream
     case 1: return launch_decode<1, D, DV, LOW>(p, grid, st);
     case 2: return launch_decode<2, D, DV, LOW>(p, grid, st);
     case 4: return launch_decode<4, D, DV, LOW>(p, grid, st);
-    case 8: return launch_decode<8, D, DV, LOW>(p, grid, st);
-    default: return launch_decode<16, D, DV, LOW>(p, grid, st);
+    default: return launch_decode<8, D, DV, LOW>(p, grid, st);
   }
 }
 

@@ -154,6 +154,43 @@ __device__ __forceinline__ float dot_pairs(const float* q, const float2 (&x)[16]
   return (a0.x + a1.x) + (a0.y + a1.y);
 }
 
+// ---- NVFP4 QK on the tensor cores (mma.sync m16n8k16, f16 in, f32 accumulate).  An
+// NVFP4 element times its E4M3 block scale has <= 6 significant bits and lies in
+// [2^-10, 2688], so both dequantized operands are exact in f16 and every product is
+// exact in the f32 accumulator -- the same arithmetic class as the FFMA path.  One
+// k16 step is exactly one NVFP4 block.
+__device__ __forceinline__ uint32_t e2m1x2_to_h2(uint32_t byte) {
+  uint32_t h;
+  asm("{\n\t.reg .b8 b;\n\tcvt.u8.u32 b, %1;\n\tcvt.rn.f16x2.e2m1x2 %0, b;\n\t}" : "=r"(h) : "r"(byte));
+  return h;
+}
+__device__ __forceinline__ uint32_t e4m3x2_to_h2(uint32_t two) {
+  uint32_t h;
+  asm("{\n\t.reg .b16 b;\n\tcvt.u16.u32 b, %1;\n\tcvt.rn.f16x2.e4m3x2 %0, b;\n\t}" : "=r"(h) : "r"(two));
+  return h;
+}
+__device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ void mma_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// the two f16x2 fragment words of one NVFP4 row for k16 step ks: bytes 8 ks + j and
+// 8 ks + 4 + j (j = lane % 4) of the packed row, times the block scale (f16x2 splat)
+__device__ __forceinline__ void nv_frag(const uint32_t (&w)[16], int ks, int j, uint32_t s2, uint32_t& f0,
+                                        uint32_t& f1) {
+  f0 = hmul2(e2m1x2_to_h2((w[2 * ks] >> (8 * j)) & 0xFFu), s2);
+  f1 = hmul2(e2m1x2_to_h2((w[2 * ks + 1] >> (8 * j)) & 0xFFu), s2);
+}
+__device__ __forceinline__ uint32_t splat_lo(uint32_t h2) { return (h2 & 0xFFFFu) | (h2 << 16); }
+__device__ __forceinline__ uint32_t splat_hi(uint32_t h2) { return (h2 >> 16) | (h2 & 0xFFFF0000u); }
+
 // shared memory: dequantized query rows (low, high) [R][D] f32, P [4 warps][R][32],
 // warp partials (m, l) [4][R] and O [4][R][DV]
 template <int R, int D, int DV, int LOW>
@@ -171,7 +208,8 @@ struct DecSmem {
   static constexpr int oQhi = oQlo + R * D * 4;
   static constexpr int oP = oQhi + R * D * 4;
   static constexpr int oML = oP + 4 * R * 32 * 4;
-  static constexpr int oBar = oML + 4 * R * 8;
+  static constexpr int oSmma = oML + 4 * R * 8;  // NVFP4 tensor-core QK: S tile [16][32] f32 per warp
+  static constexpr int oBar = oSmma + (LOW == kDecLowNV && R >= 2 ? 4 * 16 * 32 * 4 : 0);
   static constexpr int oO = oRing;  // warp partials reuse the rings once every warp is done
   static_assert(4 * R * DV * 4 <= 4 * kStages * kStage, "partials fit in the rings");
   static constexpr int kBytes = oBar + 4 * kStages * 8;
@@ -199,8 +237,7 @@ inline int dec_ctas_per_sm(int R, int D, int DV, int low) {
     case 1: by_dims(std::integral_constant<int, 1>{}); break;
     case 2: by_dims(std::integral_constant<int, 2>{}); break;
     case 4: by_dims(std::integral_constant<int, 4>{}); break;
-    case 8: by_dims(std::integral_constant<int, 8>{}); break;
-    default: by_dims(std::integral_constant<int, 16>{}); break;
+    default: by_dims(std::integral_constant<int, 8>{}); break;
   }
   const int n = (228 * 1024) / (bytes + 1024);  // 228 KB per SM, ~1 KB reserved per CTA
   return n < 1 ? 1 : (n > 4 ? 4 : n);
@@ -273,6 +310,44 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
     }
   }
   __syncthreads();
+
+  // NVFP4: this warp's A fragments (16 query rows x D, f16) for the tensor-core QK;
+  // rows beyond the CTA's valid rows are zero
+  // (R = 1 wastes 15/16 of every MMA: measured faster on the FFMA path)
+  constexpr bool kMma = LOW == kDecLowNV && R >= 2;
+  uint32_t qa[kMma ? D / 16 : 1][4];
+  if constexpr (kMma) {
+    const int j = lane & 3;
+#pragma unroll
+    for (int h8 = 0; h8 < 2; ++h8) {
+      const int r = (lane >> 2) + 8 * h8;
+      const int64_t qr = r < R ? row_of(r) : -1;
+      uint32_t w[16];
+      uint32_t sc[D / 32];  // E4M3 scale pairs
+      if (qr >= 0) {
+#pragma unroll
+        for (int i = 0; i < D / 8; ++i) w[i] = __ldg(reinterpret_cast<const uint32_t*>(p.q_lo + qr * (D / 2)) + i);
+#pragma unroll
+        for (int i = 0; i < D / 32; ++i)
+          sc[i] = __ldg(reinterpret_cast<const uint16_t*>(p.q_lo_sf + qr * (D / 16)) + i);
+      } else {
+#pragma unroll
+        for (int i = 0; i < D / 8; ++i) w[i] = 0u;
+#pragma unroll
+        for (int i = 0; i < D / 32; ++i) sc[i] = 0u;
+      }
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks) {
+        const uint32_t s2h = e4m3x2_to_h2(sc[ks >> 1]);
+        const uint32_t s2 = (ks & 1) ? splat_hi(s2h) : splat_lo(s2h);
+        uint32_t f0, f1;
+        nv_frag(*reinterpret_cast<const uint32_t(*)[16]>(&w[0]), ks, j, s2, f0, f1);
+        qa[ks][h8] = f0;      // a0 / a1: k = 2j + {0, 1}
+        qa[ks][2 + h8] = f1;  // a2 / a3: k = 2j + 8 + {0, 1}
+      }
+    }
+  }
+  float* smma = reinterpret_cast<float*>(smem + S::oSmma) + warp * 16 * 32;
 
   int64_t last = -1;  // last visible key of any row
 #pragma unroll
@@ -355,7 +430,41 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
     float s[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) s[r] = 0.f;
-    if (need_lo) {
+    if (need_lo && kMma) {
+      // S[16 rows][32 keys] = A (q_lo) x B (this group's keys), four n8 tiles of keys
+      const int j = lane & 3, n = lane >> 2;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const uint8_t* krow = stage + S::sA + (nt * 8 + n) * (D / 2);
+        uint32_t w[16];
+#pragma unroll
+        for (int i = 0; i < D / 32; ++i) {
+          const uint4 v4 = reinterpret_cast<const uint4*>(krow)[i];
+          w[4 * i] = v4.x;
+          w[4 * i + 1] = v4.y;
+          w[4 * i + 2] = v4.z;
+          w[4 * i + 3] = v4.w;
+        }
+        const uint8_t* ksf = stage + S::sAsf + (nt * 8 + n) * (D / 16);
+        float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t scl = e4m3x2_to_h2(*reinterpret_cast<const uint16_t*>(ksf + (ks & ~1)));
+          const uint32_t s2 = (ks & 1) ? splat_hi(scl) : splat_lo(scl);
+          uint32_t b0, b1;
+          nv_frag(*reinterpret_cast<const uint32_t(*)[16]>(&w[0]), ks, j, s2, b0, b1);
+          mma_16816(c, qa[ks], b0, b1);
+        }
+        // C: rows n and n + 8, keys nt * 8 + 2 j + {0, 1}
+        *reinterpret_cast<float2*>(smma + n * 32 + nt * 8 + 2 * j) = make_float2(c[0], c[1]);
+        *reinterpret_cast<float2*>(smma + (n + 8) * 32 + nt * 8 + 2 * j) = make_float2(c[2], c[3]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (!hi[r]) s[r] = smma[r * 32 + lane];
+      __syncwarp();
+    } else if (need_lo) {
       if constexpr (LOW != kDecLow8) {
         const uint8_t* row = stage + S::sA + lane * (D / 2);
         const uint8_t* sf = stage + S::sAsf + lane * (S::kAsf / 32);
