@@ -84,6 +84,9 @@ __device__ unsigned int g_trace_n[4];
 // polynomial (exp2_poly2) instead of MUFU.EX2
 constexpr int kPolyPP = DMA_PP_POLY;
 
+#ifndef DMA_PP_MAXCH8
+#define DMA_PP_MAXCH8 0
+#endif
 #ifndef DMA_PP_LATE_PV_WAIT
 #define DMA_PP_LATE_PV_WAIT 0
 #endif
@@ -799,6 +802,17 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
           for (int j = 0; j < NK; ++j)
             if (j >= lim) tv[j] = -INFINITY;
         }
+#if DMA_PP_MAXCH8
+        // row max: 8 independent FMNMX3 chains
+        float m8[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) m8[c] = fmaxf(tv[2 * c], tv[2 * c + 1]);
+#pragma unroll
+        for (int j = 16; j < NK; j += 16)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) m8[c] = ptx::fmax3(m8[c], tv[j + 2 * c], tv[j + 2 * c + 1]);
+        float mx = fmaxf(ptx::fmax3(ptx::fmax3(m8[0], m8[1], m8[2]), ptx::fmax3(m8[3], m8[4], m8[5]), m8[6]), m8[7]);
+#else
         // row max: 4 independent FMNMX3 chains
         float m4[4] = {fmaxf(tv[0], tv[1]), fmaxf(tv[2], tv[3]), fmaxf(tv[4], tv[5]), fmaxf(tv[6], tv[7])};
 #pragma unroll
@@ -809,6 +823,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
           m4[3] = ptx::fmax3(m4[3], tv[j + 6], tv[j + 7]);
         }
         float mx = fmaxf(ptx::fmax3(m4[0], m4[1], m4[2]), m4[3]);
+#endif
         if (kSplit == 2) {
           float* rb = red + ((g & 1) * 2 + x) * 256;
           rb[hh * 128 + row] = mx;
