@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
     return (static_cast<int64_t>(b) * p.heads + static_cast<int64_t>(kvh) * p.group + gq) * p.n_q + i;
   };
   int64_t qrow[R];  // row in the [B*H, n_q] query arrays, -1 = padding
-  int64_t qpos[R];  // absolute position of the row
+  int qpos[R];      // absolute position of the row (-1: padding row; positions < 2^31)
   int hs[R];        // first high tile of the row's diagonal window
   float sqq[R];
   const int sink_t = p.sink_window / p.tile_n;
@@ -279,8 +279,8 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
       const int gq = lr / static_cast<int>(p.n_q), i = lr % static_cast<int>(p.n_q);
       const int64_t h = static_cast<int64_t>(kvh) * p.group + gq;
       qrow[r] = (static_cast<int64_t>(b) * p.heads + h) * p.n_q + i;
-      qpos[r] = p.pos + i;
-      const int64_t q0 = (qpos[r] / p.tile_m) * p.tile_m;
+      qpos[r] = static_cast<int>(p.pos + i);
+      const int64_t q0 = (static_cast<int64_t>(qpos[r]) / p.tile_m) * p.tile_m;
       hs[r] = static_cast<int>(ceil_div(q0 - p.diag_window, static_cast<int64_t>(p.tile_n)));
       sqq[r] = static_cast<float>(p.q_sq[qrow[r]]);
     } else {
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
 
   int64_t last = -1;  // last visible key of any row
 #pragma unroll
-  for (int r = 0; r < R; ++r) last = qpos[r] > last ? qpos[r] : last;
+  for (int r = 0; r < R; ++r) last = qpos[r] > last ? qpos[r] : last;  // (int64 last)
   const int64_t k_begin = static_cast<int64_t>(split) * p.keys_per_split;
   int64_t k_end = k_begin + p.keys_per_split;
   k_end = k_end < last + 1 ? k_end : last + 1;
@@ -371,12 +371,12 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
 
   // which operand copies a 32-key group needs (per row: the tile's precision for that row)
   auto needs = [&](int64_t g, bool& nlo, bool& nhi) {
-    const int t = static_cast<int>(g / p.tile_n);  // a 32-key group lies in one key tile
+    const int t = static_cast<int>(static_cast<uint32_t>(g) / static_cast<uint32_t>(p.tile_n));  // one key tile per group
     nlo = nhi = false;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const bool h = LOW == kDecLow8 || t < sink_t || t >= hs[r];
-      if (qrow[r] >= 0 && g <= qpos[r]) (h ? nhi : nlo) = true;
+      if (static_cast<int>(g) <= qpos[r]) (h ? nhi : nlo) = true;  // padding rows: qpos = -1
     }
   };
   // producer side of this warp's ring (lane 0): bulk-load the 32 cache rows of group g
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
     const uint8_t* stage = ring + st * S::kStage;
     const int64_t j = g0 + lane;
     const bool in = j < k_end;
-    const int t = static_cast<int>(g0 / p.tile_n);
+    const int t = static_cast<int>(static_cast<uint32_t>(g0) / static_cast<uint32_t>(p.tile_n));
     bool hi[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) hi[r] = LOW == kDecLow8 || t < sink_t || t >= hs[r];
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
     const float sqk = static_cast<float>(reinterpret_cast<const double*>(stage + S::sSq)[lane]);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const bool vis = in && qrow[r] >= 0 && j <= qpos[r];
+      const bool vis = in && static_cast<int>(j) <= qpos[r];
       const bool use_sq = hi[r] || LOW == kDecLowNV;
       float x = use_sq ? s[r] * (sqq[r] * sqk) : s[r];
       x = vis ? x : -INFINITY;
