@@ -1,3 +1,5 @@
+#!/bin/bash
+# GPU session for the decode kernel: parity tests, six bench shapes -> gpurun_out/r01_decode.jsonl, one ncu --set full capture.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out; rm -f gpurun_out/r01_decode.jsonl
 timeout 900 python -m pytest tests/test_gpu_decode.py -x -q 2>&1 | tail -3
