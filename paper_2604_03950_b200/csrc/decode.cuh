@@ -209,7 +209,7 @@ struct DecSmem {
   static constexpr int oP = oQhi + R * D * 4;
   static constexpr int oML = oP + 4 * R * 32 * 4;
   static constexpr int oSmma = oML + 4 * R * 8;  // NVFP4 tensor-core QK: S tile [16][32] f32 per warp
-  static constexpr int oBar = oSmma + (LOW == kDecLowNV && R >= 2 ? 4 * 16 * 32 * 4 : 0);
+  static constexpr int oBar = oSmma + ((LOW == kDecLowNV || LOW == kDecLowMX4) && R >= 2 ? 4 * 16 * 32 * 4 : 0);
   static constexpr int oO = oRing;  // warp partials reuse the rings once every warp is done
   static_assert(4 * R * DV * 4 <= 4 * kStages * kStage, "partials fit in the rings");
   static constexpr int kBytes = oBar + 4 * kStages * 8;
@@ -314,8 +314,9 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
   // NVFP4: this warp's A fragments (16 query rows x D, f16) for the tensor-core QK;
   // rows beyond the CTA's valid rows are zero
   // (R = 1 wastes 15/16 of every MMA: measured faster on the FFMA path)
-  constexpr bool kMma = LOW == kDecLowNV && R >= 2;
+  constexpr bool kMma = (LOW == kDecLowNV || LOW == kDecLowMX4) && R >= 2;
   uint32_t qa[kMma ? D / 16 : 1][4];
+  float qsc[2][LOW == kDecLowMX4 ? D / 32 : 1];  // MXFP4: E8M0 block scales of rows n, n + 8
   if constexpr (kMma) {
     const int j = lane & 3;
 #pragma unroll
@@ -323,13 +324,14 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
       const int r = (lane >> 2) + 8 * h8;
       const int64_t qr = r < R ? row_of(r) : -1;
       uint32_t w[16];
-      uint32_t sc[D / 32];  // E4M3 scale pairs
+      uint32_t sc[D / 32];  // NVFP4: E4M3 scale pairs; MXFP4: E8M0 bytes
       if (qr >= 0) {
 #pragma unroll
         for (int i = 0; i < D / 8; ++i) w[i] = __ldg(reinterpret_cast<const uint32_t*>(p.q_lo + qr * (D / 2)) + i);
 #pragma unroll
         for (int i = 0; i < D / 32; ++i)
-          sc[i] = __ldg(reinterpret_cast<const uint16_t*>(p.q_lo_sf + qr * (D / 16)) + i);
+          sc[i] = LOW == kDecLowNV ? __ldg(reinterpret_cast<const uint16_t*>(p.q_lo_sf + qr * (D / 16)) + i)
+                                   : __ldg(p.q_lo_sf + qr * (D / 32) + i);
       } else {
 #pragma unroll
         for (int i = 0; i < D / 8; ++i) w[i] = 0u;
@@ -338,12 +340,21 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
       }
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks) {
-        const uint32_t s2h = e4m3x2_to_h2(sc[ks >> 1]);
-        const uint32_t s2 = (ks & 1) ? splat_hi(s2h) : splat_lo(s2h);
+        // NVFP4: element x E4M3 block scale (exact in f16); MXFP4: the raw element, the
+        // power-of-two block scale is applied to the block's f32 partial sums below
+        uint32_t s2 = 0x3C003C00u;  // f16x2 (1, 1)
+        if constexpr (LOW == kDecLowNV) {
+          const uint32_t s2h = e4m3x2_to_h2(sc[ks >> 1]);
+          s2 = (ks & 1) ? splat_hi(s2h) : splat_lo(s2h);
+        }
         uint32_t f0, f1;
         nv_frag(*reinterpret_cast<const uint32_t(*)[16]>(&w[0]), ks, j, s2, f0, f1);
         qa[ks][h8] = f0;      // a0 / a1: k = 2j + {0, 1}
         qa[ks][2 + h8] = f1;  // a2 / a3: k = 2j + 8 + {0, 1}
+      }
+      if constexpr (LOW == kDecLowMX4) {
+#pragma unroll
+        for (int b = 0; b < D / 32; ++b) qsc[h8][b] = qr >= 0 ? e8m0_to_f(sc[b]) : 0.f;
       }
     }
   }
@@ -445,15 +456,36 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
           w[4 * i + 2] = v4.z;
           w[4 * i + 3] = v4.w;
         }
-        const uint8_t* ksf = stage + S::sAsf + (nt * 8 + n) * (D / 16);
         float c[4] = {0.f, 0.f, 0.f, 0.f};
+        if constexpr (LOW == kDecLowNV) {
+          const uint8_t* ksf = stage + S::sAsf + (nt * 8 + n) * (D / 16);
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t scl = e4m3x2_to_h2(*reinterpret_cast<const uint16_t*>(ksf + (ks & ~1)));
-          const uint32_t s2 = (ks & 1) ? splat_hi(scl) : splat_lo(scl);
-          uint32_t b0, b1;
-          nv_frag(*reinterpret_cast<const uint32_t(*)[16]>(&w[0]), ks, j, s2, b0, b1);
-          mma_16816(c, qa[ks], b0, b1);
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint32_t scl = e4m3x2_to_h2(*reinterpret_cast<const uint16_t*>(ksf + (ks & ~1)));
+            const uint32_t s2 = (ks & 1) ? splat_hi(scl) : splat_lo(scl);
+            uint32_t b0, b1;
+            nv_frag(*reinterpret_cast<const uint32_t(*)[16]>(&w[0]), ks, j, s2, b0, b1);
+            mma_16816(c, qa[ks], b0, b1);
+          }
+        } else {
+          // MXFP4: per 32-column block, raw-element MMAs (2 x k16) into a fresh accumulator,
+          // then x 2^(e_q + e_k) for the accumulator's rows (n, n + 8) and keys (2j, 2j + 1)
+          const uint8_t* ksf0 = stage + S::sAsf + (nt * 8 + 2 * j) * (D / 32);
+#pragma unroll
+          for (int b = 0; b < D / 32; ++b) {
+            float cb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              uint32_t b0, b1;
+              nv_frag(*reinterpret_cast<const uint32_t(*)[16]>(&w[0]), 2 * b + h, j, 0x3C003C00u, b0, b1);
+              mma_16816(cb, qa[2 * b + h], b0, b1);
+            }
+            const float k0 = e8m0_to_f(ksf0[b]), k1 = e8m0_to_f(ksf0[D / 32 + b]);
+            c[0] = fmaf(cb[0], qsc[0][b] * k0, c[0]);
+            c[1] = fmaf(cb[1], qsc[0][b] * k1, c[1]);
+            c[2] = fmaf(cb[2], qsc[1][b] * k0, c[2]);
+            c[3] = fmaf(cb[3], qsc[1][b] * k1, c[3]);
+          }
         }
         // C: rows n and n + 8, keys nt * 8 + 2 j + {0, 1}
         *reinterpret_cast<float2*>(smma + n * 32 + nt * 8 + 2 * j) = make_float2(c[0], c[1]);

@@ -32,6 +32,8 @@ CASES = [
     ("nv_d128_T128", 700, 1, 2, 2, 128, 128, 128, 128, 128, 128, "nvfp4", "mxfp8"),
     ("nv_gqa4_nq3", 515, 3, 8, 2, 128, 128, 128, 128, 256, 0, "nvfp4", "mxfp8"),
     ("mx4_d64_t64", 333, 2, 4, 1, 64, 64, 64, 64, 64, 64, "mxfp4", "mxfp8"),
+    ("mx4_d128_gqa4_tc", 600, 1, 8, 2, 128, 128, 128, 128, 128, 128, "mxfp4", "mxfp8"),
+    ("mx4_d128_single_row", 300, 1, 2, 2, 128, 128, 128, 128, 0, 0, "mxfp4", "mxfp8"),
     ("low8_e5m2", 260, 1, 2, 1, 128, 64, 128, 128, 0, 128, "mxfp8", "e5m2"),
     ("nv_T0_S0_tile_m32", 640, 4, 4, 4, 128, 128, 32, 64, 0, 0, "nvfp4", "mxfp8"),
     ("nv_gqa16_nq1", 1100, 1, 16, 1, 128, 128, 128, 128, 128, 128, "nvfp4", "mxfp8"),

@@ -30,9 +30,11 @@ def main():
     ap.add_argument("--d", type=int, default=128)
     ap.add_argument("--nq", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--low", default="nvfp4", choices=["nvfp4", "mxfp4", "mxfp8"])
     args = ap.parse_args()
     B, H, KVH, L, d, nq = args.batch, args.heads, args.kv_heads, args.ctx, args.d, args.nq
-    cfg = D.AttentionConfig(tile_m=128, tile_n=128, diag_window=128, sink_window=128)
+    low = {"nvfp4": D.NVFP4, "mxfp4": D.MXFP4, "mxfp8": D.MXFP8_E4M3}[args.low]
+    cfg = D.AttentionConfig(tile_m=128, tile_n=128, diag_window=128, sink_window=128, low_format=low)
     cache = D.DmaKVCache(cfg, batch=B, kv_heads=KVH, capacity=L, head_dim=d)
     g = torch.Generator(device="cuda").manual_seed(0)
     for b0 in range(0, L, 8192):  # fill in chunks (bounded temporaries)
@@ -54,12 +56,13 @@ def main():
         ts.append(e0.elapsed_time(e1))
     ms = sorted(ts)[len(ts) // 2]
     hfrac_keys = min(L, 128 + 256) / L  # sink tile + the window tiles (row's q tile and the one before)
-    per_key = hfrac_keys * (d + d / 32) + (1 - hfrac_keys) * (d / 2 + d / 16) + 8 + 2 * d
+    lo_bytes = {"nvfp4": d / 2 + d / 16, "mxfp4": d / 2 + d / 32, "mxfp8": d + d / 32}[args.low]
+    per_key = hfrac_keys * (d + d / 32) + (1 - hfrac_keys) * lo_bytes + 8 + 2 * d
     nbytes = B * KVH * L * per_key + B * H * nq * (d + d / 2 + d / 16 + d / 32 + 8 + 4 * d)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     print(json.dumps({"metric": "decode_step_ms", "value": ms, "batch": B, "heads": H, "kv_heads": KVH, "ctx": L,
-                      "d": d, "n_q": nq, "bytes": nbytes, "achieved_GBps": nbytes / (ms * 1e-3) / 1e9,
+                      "d": d, "n_q": nq, "low": args.low, "bytes": nbytes, "achieved_GBps": nbytes / (ms * 1e-3) / 1e9,
                       "peaks": {k: v for k, v in peaks.items() if "hbm" in k.lower() or "copy" in k.lower()}}))
 
 
