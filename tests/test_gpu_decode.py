@@ -134,3 +134,23 @@ def test_decode_errors():
     cache.append(k[:, :, :8], k[:, :, :8])
     with pytest.raises(ValueError, match="n_q"):
         cache.attend(torch.randn(1, 1, 9, 64, device="cuda"))
+
+
+def test_decode_from_empty_cache():
+    """First tokens of a sequence: no prompt, one step of 3 tokens (causal among themselves),
+    then single tokens -- every row equals the oracle's row of the whole sequence."""
+    m = D()
+    L, H, KVH, d = 40, 2, 1, 64
+    q, k, v = (randn_bf16(900 + i, h, L, d) for i, h in enumerate((H, KVH, KVH)))
+    cfg = m.AttentionConfig(tile_m=64, tile_n=64, diag_window=64, sink_window=0)
+    cache = m.DmaKVCache(cfg, batch=1, kv_heads=KVH, capacity=L, head_dim=d)
+    qt, kt, vt = (torch.from_numpy(x).cuda()[None] for x in (q, k, v))
+    outs = [cache.step(qt[:, :, :3], kt[:, :, :3], vt[:, :, :3])]
+    for i in range(3, L):
+        outs.append(cache.step(qt[:, :, i:i + 1], kt[:, :, i:i + 1], vt[:, :, i:i + 1]))
+    got = torch.cat(outs, dim=2)[0].double().cpu().numpy()
+    ocfg = O.Cfg(tile_m=64, tile_n=64, diag_window=64, sink_window=0, causal=True, low_format=O.NVFP4,
+                 high_format=O.MXFP8_E4M3, granularity=O.TOKEN)
+    for h in range(H):
+        want = O.mixed_precision_attention(q[h], k[0], v[0], ocfg)
+        assert np.abs(got[h] - want).max() <= TOL_DECODE[1]
