@@ -208,8 +208,11 @@ struct DecSmem {
   static constexpr int oQhi = oQlo + R * D * 4;
   static constexpr int oP = oQhi + R * D * 4;
   static constexpr int oML = oP + 4 * R * 32 * 4;
-  static constexpr int oSmma = oML + 4 * R * 8;  // NVFP4 tensor-core QK: S tile [16][32] f32 per warp
-  static constexpr int oBar = oSmma + ((LOW == kDecLowNV || LOW == kDecLowMX4) && R >= 2 ? 4 * 16 * 32 * 4 : 0);
+  static constexpr bool kMma = (LOW == kDecLowNV || LOW == kDecLowMX4) && R >= 2;
+  static constexpr int oSmma = oML + 4 * R * 8;  // tensor-core QK: S tile [16][32] f32 per warp
+  // rows' S_q^Q and positions [16] (f32, i32), per-warp row maxima [4][16] (tensor-core path)
+  static constexpr int oRows = oSmma + (kMma ? 4 * 16 * 32 * 4 : 0);
+  static constexpr int oBar = oRows + (kMma ? 16 * 4 * 2 + 4 * 16 * 4 : 0);
   static constexpr int oO = oRing;  // warp partials reuse the rings once every warp is done
   static_assert(4 * R * DV * 4 <= 4 * kStages * kStage, "partials fit in the rings");
   static constexpr int kBytes = oBar + 4 * kStages * 8;
@@ -290,6 +293,22 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
       sqq[r] = 0.f;
     }
   }
+  if constexpr (S::kMma) {
+    float* rs = reinterpret_cast<float*>(smem + S::oRows);
+    int* rp = reinterpret_cast<int*>(smem + S::oRows + 64);
+    if (threadIdx.x < 16) {
+      float v = 0.f;
+      int q = -1;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r == static_cast<int>(threadIdx.x)) {
+          v = sqq[r];
+          q = qpos[r];
+        }
+      rs[threadIdx.x] = v;
+      rp[threadIdx.x] = q;
+    }
+  }
   // dequantize the query rows (block scales only; S_q folds in per logit)
   for (int idx = threadIdx.x; idx < R * (D / 32); idx += blockDim.x) {
     const int r = idx / (D / 32), c = idx % (D / 32);
@@ -314,7 +333,7 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
   // NVFP4: this warp's A fragments (16 query rows x D, f16) for the tensor-core QK;
   // rows beyond the CTA's valid rows are zero
   // (R = 1 wastes 15/16 of every MMA: measured faster on the FFMA path)
-  constexpr bool kMma = (LOW == kDecLowNV || LOW == kDecLowMX4) && R >= 2;
+  constexpr bool kMma = S::kMma;
   uint32_t qa[kMma ? D / 16 : 1][4];
   float qsc[2][LOW == kDecLowMX4 ? D / 32 : 1];  // MXFP4: E8M0 block scales of rows n, n + 8
   if constexpr (kMma) {
@@ -359,6 +378,9 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
     }
   }
   float* smma = reinterpret_cast<float*>(smem + S::oSmma) + warp * 16 * 32;
+  const float* rows_sq = reinterpret_cast<const float*>(smem + S::oRows);
+  const int* rows_pos = reinterpret_cast<const int*>(smem + S::oRows + 64);
+  float* rmax_w = reinterpret_cast<float*>(smem + S::oRows + 128) + warp * 16;
 
   int64_t last = -1;  // last visible key of any row
 #pragma unroll
@@ -441,9 +463,15 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
     float s[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) s[r] = 0.f;
+    // tensor-core groups where no row needs the high copy finish their logits and row
+    // maxima in the MMA epilogue (no per-row warp shuffles below)
+    const bool lo_only = kMma && need_lo && !need_hi;
     if (need_lo && kMma) {
       // S[16 rows][32 keys] = A (q_lo) x B (this group's keys), four n8 tiles of keys
       const int j = lane & 3, n = lane >> 2;
+      const float sq_n = rows_sq[n];
+      const int qp_n = rows_pos[n];
+      float lmax = -INFINITY;
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
         const uint8_t* krow = stage + S::sA + (nt * 8 + n) * (D / 2);
@@ -487,15 +515,37 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
             c[3] = fmaf(cb[3], qsc[1][b] * k1, c[3]);
           }
         }
-        // C: rows n and n + 8, keys nt * 8 + 2 j + {0, 1}
-        *reinterpret_cast<float2*>(smma + n * 32 + nt * 8 + 2 * j) = make_float2(c[0], c[1]);
-        *reinterpret_cast<float2*>(smma + (n + 8) * 32 + nt * 8 + 2 * j) = make_float2(c[2], c[3]);
+        // C: rows n and n + 8 (padding: R <= 8), keys nt * 8 + 2 j + {0, 1}
+        if (lo_only) {
+          // final logits here: S_q^Q S_q^K (NVFP4), causal / ragged mask, running row max
+          const int kk = nt * 8 + 2 * j;
+          const double* sqd = reinterpret_cast<const double*>(stage + S::sSq);
+          float x0 = c[0], x1 = c[1];
+          if (LOW == kDecLowNV) {
+            x0 *= sq_n * static_cast<float>(sqd[kk]);
+            x1 *= sq_n * static_cast<float>(sqd[kk + 1]);
+          }
+          const int key0 = static_cast<int>(g0) + kk;
+          x0 = (key0 < k_end && key0 <= qp_n) ? x0 : -INFINITY;
+          x1 = (key0 + 1 < k_end && key0 + 1 <= qp_n) ? x1 : -INFINITY;
+          *reinterpret_cast<float2*>(smma + n * 32 + kk) = make_float2(x0, x1);
+          lmax = fmaxf(lmax, fmaxf(x0, x1));
+        } else {
+          *reinterpret_cast<float2*>(smma + n * 32 + nt * 8 + 2 * j) = make_float2(c[0], c[1]);
+        }
+      }
+      if (lo_only) {
+        lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, 1));
+        lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, 2));
+        if (j == 0 && n < 16) rmax_w[n] = lmax;
       }
       __syncwarp();
+      if (!lo_only) {
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (!hi[r]) s[r] = smma[r * 32 + lane];
-      __syncwarp();
+        for (int r = 0; r < R; ++r)
+          if (!hi[r]) s[r] = smma[r * 32 + lane];
+        __syncwarp();
+      }
     } else if (need_lo) {
       if constexpr (LOW != kDecLow8) {
         const uint8_t* row = stage + S::sA + lane * (D / 2);
@@ -541,13 +591,21 @@ __global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode
     const float sqk = static_cast<float>(reinterpret_cast<const double*>(stage + S::sSq)[lane]);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const bool vis = in && static_cast<int>(j) <= qpos[r];
-      const bool use_sq = hi[r] || LOW == kDecLowNV;
-      float x = use_sq ? s[r] * (sqq[r] * sqk) : s[r];
-      x = vis ? x : -INFINITY;
-      float gm = x;
+      bool vis;
+      float x, gm;
+      if (lo_only) {
+        x = smma[r * 32 + lane];
+        vis = x != -INFINITY;
+        gm = rmax_w[r];
+      } else {
+        vis = in && static_cast<int>(j) <= qpos[r];
+        const bool use_sq = hi[r] || LOW == kDecLowNV;
+        x = use_sq ? s[r] * (sqq[r] * sqk) : s[r];
+        x = vis ? x : -INFINITY;
+        gm = x;
 #pragma unroll
-      for (int off = 16; off; off >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, off));
+        for (int off = 16; off; off >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, off));
+      }
       const float mn = fmaxf(m[r], gm);
       float pv = 0.f;
       if (mn != -INFINITY) {
