@@ -31,6 +31,10 @@ namespace dma {
                           // 11-13 % faster than 2 and far ahead of 3)
 #endif
 
+#ifndef DMA_DEC_MINB
+#define DMA_DEC_MINB(R) ((R) <= 4 ? 4 : ((R) <= 8 ? 3 : 2))  // min resident CTAs (register cap)
+#endif
+
 enum { kDecLowNV = 0, kDecLowMX4 = 1, kDecLow8 = 2 };
 
 struct DecodeParams {
@@ -253,7 +257,7 @@ inline int dec_ctas_per_sm(int R, int D, int DV, int low) {
 }
 
 template <int R, int D, int DV, int LOW>
-__global__ void __launch_bounds__(128, R <= 4 ? 4 : (R <= 8 ? 3 : 2)) dma_decode_kernel(const DecodeParams p) {
+__global__ void __launch_bounds__(128, DMA_DEC_MINB(R)) dma_decode_kernel(const DecodeParams p) {
   using S = DecSmem<R, D, DV, LOW>;
   extern __shared__ __align__(16) uint8_t smem[];
   float* q_lo = reinterpret_cast<float*>(smem + S::oQlo);
