@@ -17,6 +17,7 @@ Differences from the float64 reference that are intrinsic to tensor cores
 from __future__ import annotations
 
 import ctypes
+import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -171,9 +172,15 @@ class DmaAttention:
         if out is None:
             out = torch.empty((B, H, Lq, v.shape[-1]), dtype=odt, pin_memory=True)
         if chunk_kv_heads is None:
-            # >= 2 query heads (one head pair x every q tile fills the 148 SMs at N >= 8K) and
-            # up to ~16 chunks per batch element (measured best at c2 / c3: 1 / 2 KV heads)
-            chunk_kv_heads = max(1, min(KVH, max(-(-2 // (H // KVH)), KVH // 16)))
+            # about one chunk per 50 MB of Q/K/V, 4..16 chunks per call, >= 2 query heads per
+            # chunk (a head pair x every q tile fills the 148 SMs at N >= 8K).  Measured best
+            # (tools/e2e_chunks.py, e2e_var.py): c2 2 KV heads (4 chunks, 2.70 ms vs 2.87 with 1),
+            # c3 2 (16 chunks), c4 4 (8 chunks, 8.24 vs 8.71 ms with 2)
+            total = sum(t.numel() * t.element_size() for t in (q, k, v))
+            n_target = min(16, max(4, total // (50 * 2**20)))
+            want = KVH / max(1, n_target // B)
+            pow2 = 1 << max(0, round(math.log2(want))) if want >= 1 else 1  # even chunks
+            chunk_kv_heads = max(1, min(KVH, max(-(-2 // (H // KVH)), pow2)))
         # the graph pays off where the host calls outnumber the GPU work (small chunks, e.g.
         # c2: 8.9 -> 2.8 ms); with large chunks its copy nodes overlap worse than eager
         # streams (c3: 16.7 eager vs 18.2 ms graph), so big chunks run eagerly
