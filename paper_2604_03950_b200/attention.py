@@ -214,6 +214,11 @@ class DmaAttention:
         G = H // KVH
         odt = out.dtype
         units = [(b, h0, min(KVH, h0 + chunk_kv_heads)) for b in range(B) for h0 in range(0, KVH, chunk_kv_heads)]
+        if len(units) >= 4 and units[-1][2] - units[-1][1] > 1:
+            # the pipeline tail (last chunk's forward + D2H) is exposed: finish with single
+            # KV heads so it is as short as possible
+            b, h0, h1 = units.pop()
+            units += [(b, h, h + 1) for h in range(h0, h1)]
         cur = torch.cuda.current_stream()
         # streams, device buffers and per-slot workspaces persist across calls with the same
         # shapes: per-call allocations freed through record_stream kept the caching allocator
