@@ -31,6 +31,9 @@ namespace dma {
                           // 11-13 % faster than 2 and far ahead of 3)
 #endif
 
+#ifndef DMA_DEC_MMA_MIN_R
+#define DMA_DEC_MMA_MIN_R 2  // tensor-core QK from this many query rows per CTA
+#endif
 #ifndef DMA_DEC_MINB
 #define DMA_DEC_MINB(R) ((R) <= 4 ? 4 : ((R) <= 8 ? 3 : 2))  // min resident CTAs (register cap)
 #endif
@@ -212,7 +215,7 @@ struct DecSmem {
   static constexpr int kAsf = 32 * (D / (LOW == kDecLowNV ? 16 : 32));
   static constexpr int sA = 0, sAsf = kA, sSq = sAsf + kAsf, sV = sSq + 32 * 8;
   static constexpr int kStage = (sV + 32 * DV * 2 + 127) / 128 * 128;
-  static constexpr bool kMma = (LOW == kDecLowNV || LOW == kDecLowMX4) && R >= 2;
+  static constexpr bool kMma = (LOW == kDecLowNV || LOW == kDecLowMX4) && R >= DMA_DEC_MMA_MIN_R;
   static constexpr int oRing = 0;
   static constexpr int oQlo = oRing + 4 * kStages * kStage;
   // dequantized low query rows: only the FFMA low path reads them
