@@ -313,3 +313,22 @@ def test_full_length_c3_sampled_tiles(pv):
             r = slice(128 * t, 128 * t + 128)
             rel, mx = errs(got[h, r], want[r])
             assert rel <= TOL_EMU[pv][0] and mx <= TOL_EMU[pv][1], (pv, h, t, rel, mx)
+
+
+@pytest.mark.parametrize("pv", ["mxfp8", "bf16"])
+def test_float32_inputs_full_mantissa(pv):
+    """f32 Q/K/V with full-width mantissas (phase 1 quantizes them bit-exactly from f32; V
+    enters PV as MXFP8 or bf16 of the f32 values) against the oracle on the same values."""
+    import torch
+
+    rng = np.random.default_rng(21)
+    H, N, d = 2, 640, 128
+    q, k, v = (rng.standard_normal((H, N, d)).astype(np.float32) for _ in range(3))
+    c, oc = cfgs("nvfp4", "e4m3", "token", 128, 128, True, pv)
+    got = D().DmaAttention(c)(*(torch.from_numpy(x)[None].cuda() for x in (q, k, v)),
+                              out_dtype=torch.float32)[0].double().cpu().numpy()
+    for h in range(H):
+        want = O.mixed_precision_attention(q[h].astype(np.float64), k[h].astype(np.float64),
+                                           v[h].astype(np.float64), oc, pv=pv)
+        rel, mx = errs(got[h], want)
+        assert rel <= TOL_EMU[pv][0] and mx <= TOL_EMU[pv][1], (pv, h, rel, mx)

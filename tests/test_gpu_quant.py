@@ -125,3 +125,28 @@ def test_codecs_golden(golden):
         D.encode_e2m1(6.5)
     with pytest.raises(ValueError):
         D.encode_fp8(np.nan, D.E4M3)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("gran", ["token", "tensor", "block"])
+def test_quantize_dual_full_precision_inputs(dtype, gran):
+    """f32 / f64 inputs with full-width mantissas (not bf16-representable): the quant16 f32
+    path and the IEEE-division f64 path, bit-exact against the oracle, as query and as key."""
+    import torch
+
+    D = dma()
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((777, 128)) * np.exp(rng.uniform(-3, 3, size=(777, 1)))
+    x[5] = 0.0
+    x[6, :32] = 1e-30  # tiny block next to normal ones
+    xt = torch.from_numpy(x.astype(dtype)).cuda()
+    xd = xt.double().cpu().numpy()
+    G = {"token": D.Granularity.TOKEN, "tensor": D.Granularity.TENSOR, "block": D.Granularity.BLOCK}[gran]
+    for isq in (True, False):
+        t = D.quantize_dual(xt, isq, D.NVFP4, D.MXFP8_E4M3, G)
+        r = O.quantize_dual(xd, isq, O.NVFP4, O.MXFP8_E4M3, gran)
+        np.testing.assert_array_equal(t.high_codes.cpu().numpy(), r.high_codes)
+        np.testing.assert_array_equal(t.scales_high.cpu().numpy(), r.scales_high)
+        np.testing.assert_array_equal(t.packed_low.bytes_.cpu().numpy(), r.packed_low)
+        np.testing.assert_array_equal(t.scales_low.cpu().numpy(), r.scales_low)
+        np.testing.assert_array_equal(t.quant_scale.cpu().numpy().ravel(), np.asarray(r.quant_scale).ravel())
