@@ -94,3 +94,43 @@ def test_decode_fuzz(seed):
         want = O.mixed_precision_attention(q[h], k[h // G], v[h // G], ocfg)[L - nq:]
         rel = np.linalg.norm(got[h] - want) / np.linalg.norm(want)
         assert rel <= TOL_DECODE[0] and np.abs(got[h] - want).max() <= TOL_DECODE[1], (seed, h, rel)
+
+
+TOL_DEQ_EMU = {"bf16": (1e-2, 5e-2), "mxfp8": (3e-2, 0.15)}  # test_gpu_attention.py (bf16 operand route)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_bf16_operand_route_fuzz(seed):
+    """BLOCK granularity and None (identity) formats: phase 1 dequantizes the bit-exact
+    quantize_dual operands to bf16 and QK runs with kind::f16 (extra error: bf16 rounding)."""
+    m = D()
+    r = np.random.default_rng(5000 + seed)
+    tile = int(r.choice([64, 128]))
+    causal = bool(r.random() < 0.7)
+    lq = int(r.integers(1, 600))
+    lk = lq if causal else int(r.integers(1, 600))
+    d = int(r.choice([64, 128]))
+    T, S = tile * int(r.integers(0, 3)), tile * int(r.integers(0, 2))
+    pv = str(r.choice(["bf16", "mxfp8"]))
+    mode = str(r.choice(["block", "identity"]))
+    if mode == "block":
+        low = str(r.choice(["nvfp4", "mxfp4"]))
+        (lo_m, lo_o), (hi_m, hi_o) = fmts(m, low, "e4m3")
+        g_m, g_o = m.Granularity.BLOCK, "block"
+    else:
+        lo_m = lo_o = hi_m = hi_o = None
+        g_m, g_o = m.Granularity.TOKEN, "token"
+    cfg = m.AttentionConfig(tile_m=tile, tile_n=tile, diag_window=T, sink_window=S, causal=causal, low_format=lo_m,
+                            high_format=hi_m, granularity=g_m, pv_mode=pv)
+    ocfg = O.Cfg(tile_m=tile, tile_n=tile, diag_window=T, sink_window=S, causal=causal, low_format=lo_o,
+                 high_format=hi_o, granularity=g_o)
+    q, k, v = randn_bf16(seed, lq, d), randn_bf16(seed + 100, lk, d), randn_bf16(seed + 200, lk, d)
+    got = m.mixed_precision_attention(q, k, v, cfg)
+    want = O.mixed_precision_attention(q, k, v, ocfg, pv=pv)
+    rel = float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30))
+    mx = float(np.abs(got - want).max())
+    # 64-tile plans: the kernel walks 128 x 128 tiles (per-quadrant masks), so its lazy MXFP8-PV
+    # rescale points differ from the emulation's 64-tile walk (see TOL_TILE64)
+    tol = TOL_DEQ_EMU[pv] if tile == 128 or pv == "bf16" else tuple(max(a, b) for a, b in
+                                                                     zip(TOL_DEQ_EMU[pv], TOL_TILE64[pv]))
+    assert rel <= tol[0] and mx <= tol[1], (seed, mode, tile, causal, lq, lk, d, pv, rel, mx)
