@@ -58,10 +58,11 @@ __device__ unsigned long long g_prof[32];
 #endif
 
 // Optional event trace of CTA 0 (-DDMA_TRACE): clock64 << 8 | event per role
-// (0/1 softmax stream A/B, 2 MMA issuer, 3 producer), read back with dma_trace_read.
+// (0/1 softmax stream A/B, 2 MMA issuer, 3 producer; attn_sk.cuh: 0/1 WG0/WG1, 2 QK, 3 PV,
+// 4 K producer, 5 V producer), read back with dma_trace_read.
 #ifdef DMA_TRACE
-__device__ unsigned long long g_trace[4][4096];
-__device__ unsigned int g_trace_n[4];
+__device__ unsigned long long g_trace[6][4096];
+__device__ unsigned int g_trace_n[6];
 // the event index lives in a register (trace_i, declared by TRACE_DECL in each role);
 // stores are fire-and-forget, so a trace point costs a few issue slots
 #define TRACE_DECL unsigned int trace_i = 0;

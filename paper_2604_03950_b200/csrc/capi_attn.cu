@@ -9,6 +9,7 @@
 
 #include "attn.cuh"
 #include "attn_pp.cuh"
+#include "attn_sk.cuh"
 #include "common.cuh"
 #include "quant.cuh"
 
@@ -296,6 +297,18 @@ static int quantize_deq(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cuda
   return 0;
 }
 
+// DMA_ATTN_KERNEL=sk selects the split-KV experiment (attn_sk.cuh: one query tile per CTA,
+// plan entries alternating between the softmax warpgroups; measured slower)
+// instead of the ping-pong kernel (attn_pp.cuh)
+static bool use_sk_kernel() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DMA_ATTN_KERNEL");
+    v = (e && e[0] == 's' && e[1] == 'k') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStream_t st) {
   const int64_t D = a->head_dim, DV = a->v_dim;
   const bool nv = a->low_format == DMA_FMT_NVFP4;
@@ -325,8 +338,15 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
     uint8_t* sfh = ws + (isq ? L.sf_q_hi : L.sf_k_hi);
     float* qs = reinterpret_cast<float*>(ws + (isq ? L.qs_q : L.qs_k));
     if (q.rows == 0) continue;
-    if (int rc = quantize_impl(&q, sfl, sfh, qs, isq ? L.lq_pad : L.lk_pad, st, (!isq && L.pp) ? 1 : 0)) return rc;
+    const int kmode = (!isq && L.pp) ? (use_sk_kernel() ? 2 : 1) : 0;  // K operand layout of the kernel
+    if (int rc = quantize_impl(&q, sfl, sfh, qs, isq ? L.lq_pad : L.lk_pad, st, kmode)) return rc;
     g_launches += L.tensor_gran ? 2 : 1;
+    if (kmode == 2) {
+      const int64_t nt = L.mk * (L.lk_pad / 128);
+      sqk_tile_stats_kernel<<<static_cast<unsigned>((nt + 7) / 8), 256, 0, st>>>(qs, nt, L.lk_pad / 128, a->len_k);
+      DMA_LAUNCH_CHECK();
+      ++g_launches;
+    }
   }
   (void)nv;
   if (L.deq)
@@ -400,6 +420,25 @@ static int launch_pp(const AttnParams& p, const PPParams& q, cudaStream_t st) {
   DMA_LAUNCH_CHECK();
   ++g_launches;
   return 0;
+}
+
+template <int D, int DV, int LOW>
+static int launch_sk(const AttnParams& p, const SKParams& q, cudaStream_t st) {
+  using C = SKCfg<D, DV, LOW>;
+  auto kern = dma_attn_sk_kernel<D, DV, LOW>;
+  DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+  const int grid = q.n_items < num_sms() ? q.n_items : num_sms();
+  kern<<<static_cast<unsigned>(grid), C::kThreads, C::kSmemBytes, st>>>(p, q);
+  DMA_LAUNCH_CHECK();
+  ++g_launches;
+  return 0;
+}
+
+template <int D, int DV>
+static int dispatch_sk(const AttnParams& p, const SKParams& q, int low, cudaStream_t st) {
+  if (low == kLowNV) return launch_sk<D, DV, kLowNV>(p, q, st);
+  if (low == kLowMX4) return launch_sk<D, DV, kLowMX4>(p, q, st);
+  return launch_sk<D, DV, kLowHigh>(p, q, st);
 }
 
 template <int D, int DV>
@@ -477,6 +516,17 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
   p.n_items = static_cast<int>(items);
   const int low = L.deq ? kLowBF16
                         : (a->low_format == DMA_FMT_NVFP4 ? kLowNV : (a->low_format == DMA_FMT_MXFP4 ? kLowMX4 : kLowHigh));
+  if (L.pp && use_sk_kernel()) {
+    // split-KV kernel (block-scaled MXFP8 PV): one query tile per work item, plan entries
+    // alternate between the two softmax warpgroups
+    SKParams q{};
+    q.n_items = static_cast<int>(items);
+    const double kv_bytes = static_cast<double>(L.mk) * static_cast<double>(L.lk_pad) * (2.6 * static_cast<double>(D));
+    q.head_major = kv_bytes > 48.0 * 1024 * 1024;
+    q.ticket = reinterpret_cast<unsigned int*>(ws + L.ticket);
+    if (D == 64) return DV == 64 ? dispatch_sk<64, 64>(p, q, low, st) : dispatch_sk<64, 128>(p, q, low, st);
+    return DV == 64 ? dispatch_sk<128, 64>(p, q, low, st) : dispatch_sk<128, 128>(p, q, low, st);
+  }
   if (L.pp) {
     // ping-pong kernel (block-scaled MXFP8 PV): pairs of heads share one query-tile plan
     PPParams q{};
@@ -569,11 +619,11 @@ int dma_attention_fwd(const DmaAttnArgs* a, void* stream) {
 int dma_last_launch_count(void) { return g_launches; }
 
 #ifdef DMA_TRACE
-// tracing builds only: copy out and clear the CTA-0 event trace ([4][4096] + counts)
+// tracing builds only: copy out and clear the CTA-0 event trace ([6][4096] + counts)
 int dma_trace_read(unsigned long long* out, unsigned int* counts) {
-  DMA_CUDA_TRY(cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 4 * 4096));
-  DMA_CUDA_TRY(cudaMemcpyFromSymbol(counts, g_trace_n, sizeof(unsigned int) * 4));
-  static const unsigned int z[4] = {0, 0, 0, 0};
+  DMA_CUDA_TRY(cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 6 * 4096));
+  DMA_CUDA_TRY(cudaMemcpyFromSymbol(counts, g_trace_n, sizeof(unsigned int) * 6));
+  static const unsigned int z[6] = {0, 0, 0, 0, 0, 0};
   DMA_CUDA_TRY(cudaMemcpyToSymbol(g_trace_n, z, sizeof(z)));
   return 0;
 }

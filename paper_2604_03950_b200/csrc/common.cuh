@@ -219,6 +219,10 @@ __host__ __device__ __forceinline__ int perm_row(int k) {
 // S_q^K slots per 128-key tile: 4 groups of 32 (one per m), padded to 36 so the
 // four groups start in different shared-memory banks
 constexpr int kSqkTile = 144;
+// padding slots of the S_q^K block (in the permuted and in the natural layout): 140 = max
+// S_q^K of the tile (f32 bits), 141 = ~bits of the min (both written by phase 1 with
+// atomicMax on zeroed words; read by attn_sk.cuh)
+constexpr int kSqkMaxSlot = 140, kSqkMinSlot = 141;
 __host__ __device__ __forceinline__ int perm_slot(int k) { return 36 * ((k >> 3) & 3) + 8 * (k >> 5) + (k & 7); }
 
 }  // namespace dma

@@ -59,10 +59,18 @@ __device__ volatile unsigned int dbg_progress[4 * 1024];
 #else
 #define DMA_PROGRESS(role, v) do {} while (0)
 #endif
+// clock read (deadlock guard) every DMA_SPIN_CHECK spins.  1 measured fastest: the clock
+// read slows the spin down, so waiting warps take fewer issue slots from the working ones
+// (c3 attention 5.74 ms with 1, 5.80-5.95 ms with 256)
+#ifndef DMA_SPIN_CHECK
+#define DMA_SPIN_CHECK 1u
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
+  uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
+    if ((++spins & (DMA_SPIN_CHECK - 1u)) != 0u) continue;  // deadlock guard: clock read every DMA_SPIN_CHECK spins
 #ifdef DMA_DEBUG_WAITS
     if (clock64() - t0 > (1ll << 36)) {  // deadlock guard (~35 s): say which barrier, then fail loudly
       if ((threadIdx.x & 31) == 0)
@@ -236,6 +244,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
         "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
+}
+// 32 columns as four .x8 loads: each needs only 8 consecutive destination registers
+// (an .x32 load pins a 32-register aligned block, which a loop-carried fragment
+// could not be coalesced with -- the split-KV softmax spilled hundreds of bytes)
+__device__ __forceinline__ void tmem_ld32_x8(uint32_t taddr, uint32_t (&r)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[8 * q]), "=r"(r[8 * q + 1]), "=r"(r[8 * q + 2]), "=r"(r[8 * q + 3]), "=r"(r[8 * q + 4]),
+                   "=r"(r[8 * q + 5]), "=r"(r[8 * q + 6]), "=r"(r[8 * q + 7])
+                 : "r"(taddr + 8 * q));
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 

@@ -107,7 +107,9 @@ struct QuantOut {
   float* qs_f32;         // [mat, rows_pad] per-row S_q as f32 (TOKEN / TENSOR)
   uint32_t* nonfinite;
   int64_t rows_pad;      // rows rounded up to 128
-  int key_perm;          // operand rows permuted inside 128-row tiles (attn_pp.cuh), codes padded to rows_pad
+  int key_perm;          // 0: canonical rows; 1: operand rows permuted inside 128-row tiles (attn_pp.cuh);
+                         // 2: natural rows (attn_sk.cuh); 1 and 2 pad codes to rows_pad and keep S_q^K
+                         // in per-tile blocks of kSqkTile slots
 };
 
 
@@ -500,7 +502,7 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
 
   const int64_t rbase = mat * rows + row;
   // operand row of the codes / scale-factor atoms (permuted inside 128-row tiles for attn_pp)
-  const int64_t orow = out.key_perm ? ((row & ~int64_t(127)) | perm_row(static_cast<int>(row & 127))) : row;
+  const int64_t orow = out.key_perm == 1 ? ((row & ~int64_t(127)) | perm_row(static_cast<int>(row & 127))) : row;
   const int64_t cbase = out.key_perm ? mat * out.rows_pad + orow : rbase;
   const int col0 = part * 16;
   if (out.packed_low)
@@ -528,7 +530,8 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
     if (GRAN == DMA_GRAN_TENSOR && out.quant_scale && row == 0) out.quant_scale[mat] = sq;
     if (GRAN != DMA_GRAN_BLOCK && out.qs_f32) {
       if (out.key_perm)
-        out.qs_f32[(mat * (out.rows_pad >> 7) + (row >> 7)) * kSqkTile + perm_slot(static_cast<int>(row & 127))] =
+        out.qs_f32[(mat * (out.rows_pad >> 7) + (row >> 7)) * kSqkTile +
+                   (out.key_perm == 1 ? perm_slot(static_cast<int>(row & 127)) : static_cast<int>(row & 127))] =
             static_cast<float>(sq);
       else
         out.qs_f32[mat * out.rows_pad + row] = static_cast<float>(sq);
@@ -729,6 +732,38 @@ static __global__ void __launch_bounds__(256) quant_v4_bf16_kernel(const __nv_bf
     const int64_t off = ((mat * ntiles + ktile) * nchunk + (c >> 7)) * 512 + ((c & 127) & 31) * 16 +
                         ((c & 127) >> 5) * 4 + (kblk & 3);
     sf_op[off] = static_cast<uint8_t>(e[j] + 127);
+  }
+}
+
+// Split-KV experiment (attn_sk.cuh, key_perm = 2): per 128-key tile of S_q^K (natural
+// order, kSqkTile slots per tile) the max / min over the valid keys into slots kSqkMaxSlot /
+// kSqkMinSlot, and S_q^K = 1 for the padded keys of the last tile.  One warp per tile.
+static __global__ void __launch_bounds__(256) sqk_tile_stats_kernel(float* __restrict__ qs, int64_t n_tiles_total,
+                                                             int64_t rtiles, int64_t rows) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wt = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (wt >= n_tiles_total) return;
+  const int64_t tile = wt % rtiles;
+  float* blk = qs + wt * kSqkTile;
+  float vmax = 0.f, vmin = INFINITY;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = 32 * i + lane;
+    if (tile * 128 + k < rows) {
+      const float v = blk[k];
+      vmax = fmaxf(vmax, v);
+      vmin = fminf(vmin, v);
+    } else {
+      blk[k] = 1.0f;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+  }
+  if (lane == 0) {
+    reinterpret_cast<unsigned int*>(blk)[kSqkMaxSlot] = __float_as_uint(vmax);
+    reinterpret_cast<unsigned int*>(blk)[kSqkMinSlot] = ~__float_as_uint(vmin);
   }
 }
 

@@ -22,8 +22,8 @@ v = torch.randn(B, KVH, N, d, device="cuda", generator=g).to(torch.bfloat16)
 a, out = D.DmaAttention(cfg).prepare(q, k, v)
 L = _lib.lib()
 sp = _lib.stream_ptr()
-buf = (ctypes.c_ulonglong * (4 * 4096))()
-cnt = (ctypes.c_uint * 4)()
+buf = (ctypes.c_ulonglong * (6 * 4096))()
+cnt = (ctypes.c_uint * 6)()
 _lib.check(L.dma_attention_quantize(a, sp), "q")
 _lib.check(L.dma_attention_core(a, sp), "core")
 torch.cuda.synchronize()
@@ -31,7 +31,7 @@ L.dma_trace_read(buf, cnt)
 _lib.check(L.dma_attention_core(a, sp), "core")
 torch.cuda.synchronize()
 L.dma_trace_read(buf, cnt)
-arr = np.frombuffer(buf, dtype=np.uint64).reshape(4, 4096)
+arr = np.frombuffer(buf, dtype=np.uint64).reshape(6, 4096)
 ev = {}
 t0 = min(int(arr[r][0] >> 8) for r in range(4) if cnt[r])
 for r in range(4):
