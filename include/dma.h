@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define DMA_ABI_VERSION 1
+#define DMA_ABI_VERSION 2
 
 enum { DMA_OK = 0, DMA_EINVAL = -1, DMA_EUNSUPPORTED = -2 };
 
@@ -132,6 +132,9 @@ typedef struct {
   double prescale; /* log2(e)/sqrt(head_dim), float64 */
   void* workspace;
   size_t workspace_bytes;
+  /* optional (may be NULL): u32 device flag, zeroed by the call and set to 1 if Q or K holds
+   * a NaN / Inf (the reference raises ValueError there, quantize.py:142-143); ABI 2 */
+  uint32_t* nonfinite;
 } DmaAttnArgs;
 
 size_t dma_attention_workspace_bytes(const DmaAttnArgs* a);

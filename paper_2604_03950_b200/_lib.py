@@ -76,9 +76,11 @@ class DmaAttnArgs(C.Structure):
         ("prescale", C.c_double),
         ("workspace", C.c_void_p),
         ("workspace_bytes", C.c_size_t),
+        ("nonfinite", C.c_void_p),
     ]
 
 
+ABI_VERSION = 2
 _lib = None
 
 
@@ -122,6 +124,8 @@ def lib():
                      "dma_attention_supported", "dma_attention_fwd", "dma_attention_quantize",
                      "dma_attention_core", "dma_selftest_mma"):
             getattr(L, name).restype = C.c_int
+        if L.dma_abi_version() != ABI_VERSION:
+            raise DmaError(f"{LIB_PATH}: ABI {L.dma_abi_version()} != {ABI_VERSION} expected: rebuild with `make`")
         _lib = L
     return _lib
 

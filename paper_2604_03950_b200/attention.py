@@ -102,15 +102,24 @@ def _args(cfg, q, k, v, o, B, H, KVH, Lq, Lk, D, DV, out_dtype):
     return a
 
 
+_NONFINITE_MSG = "quantize_dual: input contains non-finite values"
+
+
 class DmaAttention:
     """Reusable forward for fixed shapes: owns the phase-1 workspace.
 
-    q [B, H, Lq, D], k/v [B, KVH, Lk, D|DV] CUDA tensors (bf16/f32/f64).
+    q [B, H, Lq, D], k/v [B, KVH, Lk, D|DV] CUDA tensors (bf16/f32/f64), contiguous,
+    one dtype, one device.  ``validate=True`` adds the reference's non-finite check
+    (quantize.py:142-143: ValueError if Q or K holds NaN / Inf): phase 1 raises a
+    device flag and the call reads it back (one 4-byte D2H + stream sync per call);
+    the default leaves the forward asynchronous.
     """
 
-    def __init__(self, cfg: AttentionConfig):
+    def __init__(self, cfg: AttentionConfig, validate: bool = False):
         self.cfg = cfg
+        self.validate = validate
         self._ws = None
+        self._flag = None
 
     def workspace_for(self, a):
         import torch
@@ -121,32 +130,68 @@ class DmaAttention:
         return self._ws
 
     def prepare(self, q, k, v, out=None, out_dtype=None):
+        """Validate the operands and build the C-ABI arguments.  The library takes raw
+        pointers without strides, so layout mismatches are errors here, not silent."""
         import torch
 
+        if q.dim() != 4 or k.dim() != 4 or v.dim() != 4:
+            raise ValueError("Q, K, V must be 4-D [B, H, L, D] (use dma_attention for 2-D / 3-D inputs)")
         B, H, Lq, D = q.shape
         _, KVH, Lk, _ = k.shape
         DV = v.shape[-1]
         _check_qkv(q.shape, k.shape, v.shape, self.cfg.causal)
+        if k.shape[0] != B or v.shape[0] != B or v.shape[1] != KVH:
+            raise ValueError(f"batch / kv-head mismatch: Q {tuple(q.shape)}, K {tuple(k.shape)}, V {tuple(v.shape)}")
         if (self.cfg.low_format or self.cfg.high_format) and D % 32:
             raise ValueError(f"head dim {D} not divisible by 32")
         if H % KVH:
             raise ValueError(f"heads {H} not divisible by kv_heads {KVH}")
+        for name, t in (("Q", q), ("K", k), ("V", v)):
+            if not t.is_cuda or t.device != q.device:
+                raise ValueError(f"{name} must be a CUDA tensor on {q.device}, got {t.device}")
+            if not t.is_contiguous():
+                raise ValueError(f"{name} must be contiguous [B, H, L, D] (e.g. .transpose(1, 2).contiguous())")
+        if not (q.dtype == k.dtype == v.dtype):
+            raise ValueError(f"Q, K, V dtypes differ: {q.dtype}, {k.dtype}, {v.dtype}")
         odt = out_dtype or (torch.bfloat16 if q.dtype == torch.bfloat16 else torch.float32)
         if out is None:
             out = torch.empty((B, H, Lq, DV), dtype=odt, device=q.device)
+        if out.dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError(f"out dtype must be bfloat16 or float32, got {out.dtype}")
+        if tuple(out.shape) != (B, H, Lq, DV) or not out.is_contiguous() or out.device != q.device:
+            raise ValueError(f"out must be a contiguous {q.device} tensor of shape {(B, H, Lq, DV)}")
         code = _lib.DT_BF16 if out.dtype == torch.bfloat16 else _lib.DT_F32
         a = _args(self.cfg, q, k, v, out, B, H, KVH, Lq, Lk, D, DV, code)
         rc = _lib.lib().dma_attention_supported(a)
         _lib.check(rc, "dma_attention")
         ws = self.workspace_for(a)
         a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
+        if self.validate:
+            if self._flag is None or self._flag.device != q.device:
+                self._flag = torch.zeros(1, dtype=torch.int32, device=q.device)
+            a.nonfinite = self._flag.data_ptr()
         return a, out
+
+    def _check_finite(self, q, k, stream=None):
+        """After a validate=True launch: raise like quantize_dual on NaN / Inf in Q or K."""
+        import torch
+
+        if q.shape[-2] == 0 or k.shape[-2] == 0:  # no phase 1 ran: check on the device directly
+            bad = not (bool(torch.isfinite(q).all()) and bool(torch.isfinite(k).all()))
+        else:
+            s = stream if stream is not None else torch.cuda.current_stream()
+            with torch.cuda.stream(s):
+                bad = int(self._flag.item()) != 0
+        if bad:
+            raise ValueError(_NONFINITE_MSG)
 
     def __call__(self, q, k, v, out=None, out_dtype=None, stream=None):
         if not q.is_cuda:
             return self.forward_host(q, k, v, out=out, out_dtype=out_dtype)
         a, out = self.prepare(q, k, v, out, out_dtype)
         _lib.check(_lib.lib().dma_attention_fwd(a, _lib.stream_ptr(stream)), "dma_attention")
+        if self.validate:
+            self._check_finite(q, k, stream)
         return out
 
     def forward_host(self, q, k, v, out=None, out_dtype=None, chunk_kv_heads=None, graph=True):
@@ -185,11 +230,18 @@ class DmaAttention:
         # c2: 8.9 -> 2.8 ms); with large chunks its copy nodes overlap worse than eager
         # streams (c3: 16.7 eager vs 18.2 ms graph), so big chunks run eagerly
         chunk_bytes = chunk_kv_heads * Lk * D * q.element_size() * (H // KVH + 2)
-        if not graph or chunk_bytes > 24 * 2**20:
+        # copies from pageable memory cannot be captured: graphs only for pinned host tensors
+        pinned = all(t.is_pinned() for t in (q, k, v, out))
+        if not graph or not pinned or chunk_bytes > 24 * 2**20:
             self._host_pipeline(q, k, v, out, chunk_kv_heads)
+            if self.validate:
+                self._check_finite_host(q, k)
             return out
-        key = tuple((t.data_ptr(), tuple(t.shape), t.dtype) for t in (q, k, v, out)) + (chunk_kv_heads,)
-        graphs = self.__dict__.setdefault("_graphs", {})
+        # a captured graph points into the pipe entry's device buffers and workspaces, so
+        # it lives IN that entry: evicting the entry drops its graphs with the buffers
+        entry = self._pipe_entry(q, k, v, out, chunk_kv_heads)
+        graphs = entry[4]
+        key = tuple((t.data_ptr(), tuple(t.shape), t.dtype) for t in (q, k, v, out))
         g = graphs.get(key)
         if g is None:
             self._host_pipeline(q, k, v, out, chunk_kv_heads)  # eager run: allocations, checks
@@ -201,9 +253,43 @@ class DmaAttention:
                 graphs.pop(next(iter(graphs)))
             graphs[key] = g
             torch.cuda.synchronize()
-            return out
-        g.replay()
+        else:
+            g.replay()
+        if self.validate:
+            self._check_finite_host(q, k)
         return out
+
+    def _check_finite_host(self, q, k):
+        import torch
+
+        if not (bool(torch.isfinite(q).all()) and bool(torch.isfinite(k).all())):
+            raise ValueError(_NONFINITE_MSG)
+
+    def _pipe_entry(self, q, k, v, out, chunk_kv_heads):
+        """Streams, device buffers, per-slot forwards and captured graphs of one shape."""
+        import torch
+
+        B, H, Lq, D = q.shape
+        _, KVH, Lk, _ = k.shape
+        DV = v.shape[-1]
+        G = H // KVH
+        c0 = chunk_kv_heads
+        key = (B, H, KVH, Lq, Lk, D, DV, q.dtype, k.dtype, v.dtype, out.dtype, c0)
+        pipes = self.__dict__.setdefault("_pipes", {})
+        if key not in pipes:
+            n_units = B * -(-KVH // c0)
+            streams = (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream())
+            bufs, fwds = [], []
+            for _ in range(min(2, n_units)):
+                bufs.append((torch.empty((1, c0 * G, Lq, D), dtype=q.dtype, device="cuda"),
+                             torch.empty((1, c0, Lk, D), dtype=k.dtype, device="cuda"),
+                             torch.empty((1, c0, Lk, DV), dtype=v.dtype, device="cuda"),
+                             torch.empty((1, c0 * G, Lq, DV), dtype=out.dtype, device="cuda")))
+                fwds.append(DmaAttention(self.cfg))
+            if len(pipes) >= 2:
+                pipes.pop(next(iter(pipes)))  # its graphs (entry[4]) go with it
+            pipes[key] = (streams, bufs, fwds, [False], {})
+        return pipes[key]
 
     def _host_pipeline(self, q, k, v, out, chunk_kv_heads):
         import torch
@@ -212,7 +298,6 @@ class DmaAttention:
         _, KVH, Lk, _ = k.shape
         DV = v.shape[-1]
         G = H // KVH
-        odt = out.dtype
         units = [(b, h0, min(KVH, h0 + chunk_kv_heads)) for b in range(B) for h0 in range(0, KVH, chunk_kv_heads)]
         if len(units) >= 4 and units[-1][2] - units[-1][1] > 1:
             # the pipeline tail (last chunk's forward + D2H) is exposed: finish with single
@@ -223,22 +308,7 @@ class DmaAttention:
         # streams, device buffers and per-slot workspaces persist across calls with the same
         # shapes: per-call allocations freed through record_stream kept the caching allocator
         # growing and now and then stalled a call on cudaMalloc / cudaFree (17 ms -> 30-100 ms)
-        c0 = chunk_kv_heads
-        key = (B, H, KVH, Lq, Lk, D, DV, q.dtype, k.dtype, v.dtype, odt, c0)
-        pipes = self.__dict__.setdefault("_pipes", {})
-        if key not in pipes:
-            streams = (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream())
-            bufs, fwds = [], []
-            for _ in range(min(2, len(units))):
-                bufs.append((torch.empty((1, c0 * G, Lq, D), dtype=q.dtype, device="cuda"),
-                             torch.empty((1, c0, Lk, D), dtype=k.dtype, device="cuda"),
-                             torch.empty((1, c0, Lk, DV), dtype=v.dtype, device="cuda"),
-                             torch.empty((1, c0 * G, Lq, DV), dtype=odt, device="cuda")))
-                fwds.append(DmaAttention(self.cfg))
-            if len(pipes) >= 2:
-                pipes.pop(next(iter(pipes)))
-            pipes[key] = (streams, bufs, fwds, [False])
-        (s_in, s_cmp, s_out), bufs, fwds, marked = pipes[key]
+        (s_in, s_cmp, s_out), bufs, fwds, marked, _ = self._pipe_entry(q, k, v, out, chunk_kv_heads)
         # every stream starts after the caller's prior work and after all of the previous call
         for st in (s_in, s_cmp, s_out):
             st.wait_stream(cur)
@@ -280,17 +350,23 @@ class DmaAttention:
             cur.wait_stream(st)
 
 
-def dma_attention(q, k, v, cfg: AttentionConfig, out=None, out_dtype=None, stream=None):
-    """Batched forward on CUDA tensors [B, H, L, D] (also accepts [H, L, D] / [L, D])."""
+def dma_attention(q, k, v, cfg: AttentionConfig, out=None, out_dtype=None, stream=None, validate=True):
+    """Batched forward on CUDA tensors [B, H, L, D] (also accepts [H, L, D] / [L, D]).
+
+    Functional drop-in: any layout (made contiguous), K / V cast to Q's dtype, and by
+    default the reference's ValueError on non-finite Q / K (``validate``)."""
     nd = q.dim()
     if nd not in (2, 3, 4):
         raise ValueError("Q, K, V must be 2-D, 3-D or 4-D")
+    if not (k.dim() == nd and v.dim() == nd):
+        raise ValueError("Q, K, V must have the same number of dimensions")
     while q.dim() < 4:
         q, k, v = q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0)
     q, k, v = (to_device(t) for t in (q, k, v))
     if not (q.dtype == k.dtype == v.dtype):
         k, v = k.to(q.dtype), v.to(q.dtype)
-    o = DmaAttention(cfg)(q, k, v, out=out, out_dtype=out_dtype, stream=stream)
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    o = DmaAttention(cfg, validate=validate)(q, k, v, out=out, out_dtype=out_dtype, stream=stream)
     while o.dim() > nd:
         o = o.squeeze(0)
     return o
@@ -310,9 +386,9 @@ def mixed_precision_attention(q, k, v, cfg: AttentionConfig):
         raise ValueError(f"head dim {q.shape[1]} not divisible by 32")
     for x in (q, k):
         if not np.all(np.isfinite(x)):
-            raise ValueError("quantize_dual: input contains non-finite values")
+            raise ValueError(_NONFINITE_MSG)
     import torch
 
     o = dma_attention(*(torch.from_numpy(np.ascontiguousarray(x)) for x in (q, k, v)), cfg,
-                      out_dtype=torch.float32)
+                      out_dtype=torch.float32, validate=False)
     return from_device(o).astype(np.float64)

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -279,6 +280,7 @@ static int quantize_deq(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cuda
       q.quant_scale = reinterpret_cast<double*>(ws + L.r_qs[w]);
       q.workspace = L.tensor_gran ? ws + (isq ? L.absmax_q : L.absmax_k) : nullptr;
       q.workspace_bytes = L.tensor_gran ? nmat * 8 : 0;
+      q.nonfinite = a->nonfinite;
       if (int rc = quantize_impl(&q, nullptr, nullptr, nullptr, 0, st, 0)) return rc;
       g_launches += L.tensor_gran ? 2 : 1;
     }
@@ -315,6 +317,7 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
   // padded SF atoms / S_q entries must be finite: zero the small region once per call
   DMA_CUDA_TRY(cudaMemsetAsync(ws + L.small_begin, 0, L.small_end - L.small_begin, st));
   ++g_launches;
+  if (a->nonfinite) DMA_CUDA_TRY(cudaMemsetAsync(a->nonfinite, 0, sizeof(uint32_t), st));
   for (int which = 0; which < 2 && !L.deq; ++which) {
     const bool isq = which == 0;
     DmaQuantArgs q{};
@@ -334,6 +337,7 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
     q.high_codes = ws + (isq ? L.q_hi : L.k_hi);
     q.workspace = L.tensor_gran ? ws + (isq ? L.absmax_q : L.absmax_k) : nullptr;
     q.workspace_bytes = L.tensor_gran ? q.n_mat * 8 : 0;
+    q.nonfinite = a->nonfinite;
     uint8_t* sfl = L.low_fp4 ? ws + (isq ? L.sf_q_lo : L.sf_k_lo) : nullptr;
     uint8_t* sfh = ws + (isq ? L.sf_q_hi : L.sf_k_hi);
     float* qs = reinterpret_cast<float*>(ws + (isq ? L.qs_q : L.qs_k));
@@ -385,12 +389,16 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
 }
 
 static int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  // per device (SM counts are cached; the attribute query is a driver call)
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
 }

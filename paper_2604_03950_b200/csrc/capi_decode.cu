@@ -1,4 +1,5 @@
 // C-ABI: decode attention over an MX-quantized key cache (decode.cuh).
+#include <atomic>
 #include "common.cuh"
 #include "decode.cuh"
 
@@ -88,12 +89,16 @@ template <int R, int D, int DV, int LOW>
 static cudaError_t launch_decode(const DecodeParams& p, int grid, cudaStream_t st) {
   constexpr int smem = DecSmem<R, D, DV, LOW>::kBytes;
   static_assert(smem <= 227 * 1024, "decode smem");
-  static bool attr = false;
-  if (!attr) {
+  // the attribute is per device context: remember it per device (bit d), thread-safely
+  static std::atomic<unsigned long long> attr_set{0ull};
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  const unsigned long long bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (!bit || !(attr_set.load(std::memory_order_acquire) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(dma_decode_kernel<R, D, DV, LOW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr_set.fetch_or(bit, std::memory_order_release);
   }
   dma_decode_kernel<R, D, DV, LOW><<<grid, 128, smem, st>>>(p);
   return cudaGetLastError();

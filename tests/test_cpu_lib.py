@@ -27,7 +27,7 @@ def test_library_exports_header_symbols():
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(_lib.EXPORTED_SYMBOLS)
-    assert L.dma_abi_version() == 1
+    assert L.dma_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_plan_helper_matches_oracle(golden):
