@@ -2,7 +2,7 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 PKG := paper_2604_03950_b200
 SRC := $(wildcard $(PKG)/csrc/*.cu)
-HDR := $(wildcard $(PKG)/csrc/*.cuh) include/dma.h
+HDR := $(wildcard $(PKG)/csrc/*.cuh) $(PKG)/csrc/launch.h include/dma.h
 OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 LIB := $(PKG)/libdma.so
 

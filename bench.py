@@ -37,6 +37,7 @@ CONFIGS = {
     "c3": (1, 32, 32, 32768, 128, "nvfp4", 128, 128),
     "c4": (1, 32, 32, 16384, 128, "nvfp4", 128, 128),
     "c5": (1, 64, 64, 131072, 128, "nvfp4", 128, 128),  # per-rank slice of B=8 H=64
+    "c5s": (8, 64, 64, 131072, 128, "nvfp4", 128, 128),  # the whole B=8 H=64, split over the ranks
 }
 DESC = {
     "c1": "single-head DMA forward B1 H1 N1024 d64 MXFP8 diag + MXFP4 off-diag causal",
@@ -44,6 +45,7 @@ DESC = {
     "c3": "long-context prefill B1 H32 N32768 d128 causal MXFP8 diag/sink + NVFP4 off-diag",
     "c4": "window ablation point N16384 d128 T=S=128 NVFP4",
     "c5": "128K prefill H64 N131072 d128 (one batch element per rank)",
+    "c5s": "batched 128K prefill B8 H64 N131072 d128 sharded by batch x head across the ranks",
 }
 
 
@@ -128,57 +130,167 @@ def gpu_local_affinity(dev):
         return None
 
 
-def cpu_baseline(cfg_name, max_n=32768):
-    """Time the oracle port (oracle/, numpy float64) on one (b, h) head of the workload
-    (sequence capped at ``max_n`` to bound the CPU time; TFLOPS is per-FLOP, so the
-    sample's throughput stands for the whole workload)."""
-    from oracle import mx_oracle as O
-    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
-    from inputs import randn_bf16
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
+
+def _ref_head(job):
+    """One (b, h) head of the workload through the reference's own public API
+    (``mxattn.attention.mixed_precision_attention``, attention.py:282) when the unmodified
+    reference is installed in baseline/_ref, else through the oracle port (oracle/)."""
+    cfg_name, n, seed, kind = job
     B, H, KVH, N, d, low, T, S = CONFIGS[cfg_name]
-    n = N
-    cfg = O.Cfg(tile_m=128, tile_n=128, diag_window=T, sink_window=S, causal=True,
-                low_format={"nvfp4": O.NVFP4, "mxfp4": O.MXFP4}[low], high_format=O.MXFP8_E4M3)
-    n = min(N, max_n)
-    q, k, v = randn_bf16(1, n, d), randn_bf16(2, n, d), randn_bf16(3, n, d)
+    rng = np.random.default_rng(seed)
+    # bf16-representable N(0,1) inputs (the GPU arm's inputs are bf16)
+    q, k, v = ((rng.standard_normal((n, d), dtype=np.float32).view(np.uint32) & 0xFFFF0000).view(np.float32)
+               for _ in range(3))
     t0 = time.perf_counter()
-    O.mixed_precision_attention(q, k, v, cfg)
-    dt = time.perf_counter() - t0
-    f = causal_flops(1, 1, n, d)
-    cores = len(os.sched_getaffinity(0))
-    return {"value": f / dt / 1e12, "unit": "TFLOPS", "cores": cores, "kind": "port",
-            "sample": f"1 head N={n} d={d} of {cfg_name} through oracle/mx_oracle.py "
-                      f"(numpy f64, BLAS threads={cores}): {dt:.2f} s; TFLOPS = its FLOPs / time",
-            "seconds": dt}
+    if kind == "reference":
+        sys.path.insert(0, REF_DIR)
+        from mxattn import attention as RA, formats as RF
+        cfg = RA.AttentionConfig(tile_m=128, tile_n=128, diag_window=T, sink_window=S, causal=True,
+                                 low_format={"nvfp4": RF.NVFP4, "mxfp4": RF.MXFP4}[low],
+                                 high_format=RF.MXFP8_E4M3)
+        RA.mixed_precision_attention(q, k, v, cfg)
+    else:
+        from oracle import mx_oracle as O
+        cfg = O.Cfg(tile_m=128, tile_n=128, diag_window=T, sink_window=S, causal=True,
+                    low_format={"nvfp4": O.NVFP4, "mxfp4": O.MXFP4}[low], high_format=O.MXFP8_E4M3)
+        O.mixed_precision_attention(q, k, v, cfg)
+    return time.perf_counter() - t0
+
+
+def _ref_kind():
+    return "reference" if os.path.isdir(os.path.join(REF_DIR, "mxattn")) else "port"
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class RefPool:
+    """The reference's CPU path on all host cores: one worker process per core (BLAS
+    single-threaded; the reference's per-tile 128x128 GEMMs do not thread), each running
+    whole heads of the workload through ``mixed_precision_attention``."""
+
+    def __init__(self, procs=None):
+        import multiprocessing as mp
+
+        self.cores = len(os.sched_getaffinity(0))
+        self.procs = procs or self.cores
+        for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[var] = "1"
+        self.pool = mp.get_context("spawn").Pool(self.procs)
+
+    def run(self, cfg_name, n, heads, kind, seed0=0):
+        """Runs ``heads`` heads of length n; returns (wall seconds, per-head seconds)."""
+        t0 = time.perf_counter()
+        per = self.pool.map(_ref_head, [(cfg_name, n, seed0 + i, kind) for i in range(heads)], chunksize=1)
+        return time.perf_counter() - t0, per
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_baseline(cfg_name, ref_n=32768):
+    """The reference's CPU path timed on this box's host cores: one batch of heads of the
+    workload (one head per core, sequence capped at ``ref_n``) through the unmodified
+    reference (baseline/_ref; ``kind`` "reference") or the oracle port (``kind`` "port")."""
+    B, H, KVH, N, d, low, T, S = CONFIGS[cfg_name]
+    n = min(N, ref_n)
+    kind = _ref_kind()
+    pool = RefPool()
+    try:
+        pool.run(cfg_name, min(n, 1024), pool.procs, kind)  # worker start-up + imports
+        heads = pool.procs
+        wall, per = pool.run(cfg_name, n, heads, kind, seed0=100)
+    finally:
+        pool.close()
+    f = causal_flops(1, heads, n, d)
+    return {"value": f / wall / 1e12, "unit": "TFLOPS", "cores": pool.procs, "kind": kind,
+            "sample": f"{heads} heads of {cfg_name} (N={n} d={d}), one per worker process, through "
+                      f"{'mxattn.attention.mixed_precision_attention (baseline/_ref)' if kind == 'reference' else 'oracle/mx_oracle.py'}"
+                      f" on {pool.procs} host cores ({_cpu_model()}): {wall:.2f} s wall, "
+                      f"{float(np.mean(per)):.2f} s per head; TFLOPS = the heads' FLOPs / wall",
+            "seconds": wall}
 
 
 def run_reference(args, rank):
+    """``--impl reference``: the reference's own CPU implementation on the host cores, rank 0 only.
+    Steps are heads of the workload at N = min(N, --ref-n) fed to a pool of one worker per core;
+    the timed region covers exactly ``steps`` heads (pipelined over the pool)."""
     cfg_name = args.config
     if rank != 0:
         return
     B, H, KVH, N, d, low, T, S = CONFIGS[cfg_name]
-    vals = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_baseline(cfg_name, max_n=args.ref_n)
-        if i >= args.warmup:
-            vals.append(r)
-    v = float(np.mean([r["value"] for r in vals]))
-    sec = float(np.mean([r["seconds"] for r in vals]))
+    n = min(N, args.ref_n)
+    kind = _ref_kind()
+    pool = RefPool()
+    try:
+        pool.run(cfg_name, min(n, 1024), pool.procs, kind)  # worker start-up + imports (untimed)
+        if args.warmup:
+            pool.run(cfg_name, n, min(args.warmup, pool.procs), kind, seed0=10)
+        wall, per = pool.run(cfg_name, n, args.steps, kind, seed0=100)
+    finally:
+        pool.close()
+    # aggregate over the pool = workers x the per-worker rate (every head is timed inside its
+    # worker while the pool is busy); a plain flops / wall would charge the reference for the idle
+    # workers of a last, partial round when steps is not a multiple of the worker count
+    f = causal_flops(1, 1, n, d)
+    v = min(pool.procs, args.steps) * f * args.steps / float(np.sum(per)) / 1e12
+    sample = (f"{args.steps} heads of {cfg_name} (N={n} d={d}) through "
+              f"{'mxattn.attention.mixed_precision_attention (unmodified reference, baseline/_ref)' if kind == 'reference' else 'oracle/mx_oracle.py (port)'}"
+              f", one head per worker on {pool.procs} host cores ({_cpu_model()}); {wall:.1f} s wall, "
+              f"{float(np.mean(per)):.2f} s per head; TFLOPS = min(workers, steps) x head FLOPs / mean head time")
     line = {
         "metric": METRIC, "impl": "reference", "value": v, "unit": "TFLOPS", "n_gpus": args.gpus,
-        "steps": len(vals), "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg_name, "desc": DESC[cfg_name],
-                   "sample": f"one (b,h) head at N={min(N, args.ref_n)} per step (CPU-bounded sample)"},
-        "cpu_baseline": {k: vals[-1][k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": causal_flops(1, 1, n, d) / v / 1e9,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (bf16-representable N(0,1), seeded)",
+        "config": config_dict(args, 1),
+        "cpu_baseline": {"value": v, "unit": "TFLOPS", "cores": pool.procs, "kind": kind, "sample": sample},
         "e2e": {"value": v, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    line["cpu_baseline"]["value"] = v
     print(json.dumps(line), flush=True)
 
 
 METRIC = "DMA attn fwd TFLOPS & ms/call per B200 (N=8K-128K, d=128), 1/2/4/8 GPUs"
+
+
+STRONG = {"c5s"}  # global problem fixed, split by (b, kv-head) over the ranks
+
+
+def config_dict(args, world):
+    B, H, KVH, N, d, low, T, S = CONFIGS[args.config]
+    strong = args.config in STRONG
+    return {"workload": args.config, "desc": DESC[args.config],
+            ("batch_global" if strong else "batch_per_rank"): B, "heads": H, "kv_heads": KVH, "seq_len": N,
+            "head_dim": d, "tile": 128, "diag_window": T, "sink_window": S, "pv_mode": args.pv,
+            "parallelism": (f"(b, kv-head) units split over {world} rank(s) (strong); NCCL all_gather of O "
+                            f"outside the hot path" if strong else
+                            f"batch x head sharding, {world} rank(s), each with its own batch element(s) "
+                            f"(weak); no hot-path collective"),
+            "l2": "inputs exceed the 126 MB L2 (c3: 805 MB bf16 Q/K/V); no flush"}
+
+
+def self_launch(args):
+    """``--gpus N`` (N > 1) started outside torchrun: re-run this script as N ranks
+    (one process per GPU) and return its exit code; rank 0 prints the JSON line."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -191,17 +303,25 @@ def main():
     ap.add_argument("--impl", default="dma", choices=["dma", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--ref-n", type=int, default=8192, help="sequence length of one reference step's sample head")
+    ap.add_argument("--ref-n", type=int, default=32768, help="sequence length of the reference arm's sample heads")
+    ap.add_argument("--dry", action="store_true",
+                    help="launcher / sharding / gather plumbing on CPU (gloo) with a stand-in compute; "
+                         "prints the same JSON line shape (tests only, not a measurement)")
     args = ap.parse_args()
     if args.impl != "reference":
         args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
         run_reference(args, rank)
+        return
+    if args.dry:
+        run_dry(args, world, rank)
         return
 
     import torch
@@ -213,15 +333,25 @@ def main():
 
     import paper_2604_03950_b200 as D
     from paper_2604_03950_b200 import _lib
+    from paper_2604_03950_b200.sharding import gather, plan_shard
 
     B, H, KVH, N, d, low, T, S = CONFIGS[args.config]
+    strong = args.config in STRONG
+    if strong:
+        shard = plan_shard(B, H, KVH, world, rank)
+        lb, lh, lkv = 1, (shard.stop - shard.start) * shard.group, shard.stop - shard.start
+        F_total = causal_flops(B, H, N, d)
+    else:
+        shard = plan_shard(world * B, H, KVH, world, rank) if world > 1 else None
+        lb, lh, lkv = B, H, KVH
+        F_total = world * causal_flops(B, H, N, d)
     cfg = D.AttentionConfig(tile_m=128, tile_n=128, diag_window=T, sink_window=S, causal=True,
                             low_format={"nvfp4": D.NVFP4, "mxfp4": D.MXFP4}[low], high_format=D.MXFP8_E4M3,
                             granularity=D.Granularity.TOKEN, pv_mode=args.pv)
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    q = torch.randn(B, H, N, d, device="cuda", generator=g).to(torch.bfloat16)
-    k = torch.randn(B, KVH, N, d, device="cuda", generator=g).to(torch.bfloat16)
-    v = torch.randn(B, KVH, N, d, device="cuda", generator=g).to(torch.bfloat16)
+    q = torch.randn(lb, lh, N, d, device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn(lb, lkv, N, d, device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn(lb, lkv, N, d, device="cuda", generator=g).to(torch.bfloat16)
     fwd = D.DmaAttention(cfg)
     a, out = fwd.prepare(q, k, v, out_dtype=torch.bfloat16)
     L = _lib.lib()
@@ -256,18 +386,34 @@ def main():
     total_ms = ev[0][0].elapsed_time(ev[-1][2])
     quant_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
     core_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
-    launches_per_step = L.dma_last_launch_count()  # memset + Q/K/V quantize kernels + attention kernel
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    launches_per_step = L.dma_last_launch_count()  # kernels of one forward (phase 1 + attention)
+    t = torch.tensor([total_ms, quant_ms, core_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms, quant_ms, core_ms = (float(x) for x in t.tolist())
     ms_per_step = total_ms / args.steps
-    F = causal_flops(B, H, N, d)
-    value = world * F / (ms_per_step * 1e-3) / 1e12
+    value = F_total / (ms_per_step * 1e-3) / 1e12
+
+    # ---- output gather (strong scaling): NCCL all_gather of O, timed apart from the hot path
+    gather_ms = None
+    if strong and world > 1:
+        gather(out, shard, B, H)
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(3):
+            o_full = gather(out, shard, B, H)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        del o_full
+        tg = torch.tensor([g0.elapsed_time(g1) / 3], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        gather_ms = float(tg.item())
 
     # ---- end to end through the public API: pinned host Q/K/V -> H2D -> forward -> D2H O
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not strong:
         # host buffers on the GPU's NUMA node (first touch by a thread bound to its CPUs):
         # pinned memory on the far socket measured ~30% slower H2D on these boxes
         saved_aff = gpu_local_affinity(local)
@@ -275,12 +421,6 @@ def main():
         ho = torch.empty(out.shape, dtype=out.dtype).pin_memory()
         dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
         e2e_steps = max(5, min(args.steps, 9))
-
-        shard = None
-        if world > 1:
-            # global problem = one batch element per rank; O is reassembled on every rank
-            from paper_2604_03950_b200.sharding import gather, plan_shard
-            shard = plan_shard(world * B, H, KVH, world, rank)
 
         def e2e_step():
             if shard is None:
@@ -314,7 +454,7 @@ def main():
             os.sched_setaffinity(0, saved_aff)
         h2d = sum(x.numel() * x.element_size() for x in (q, k, v))
         d2h = out.numel() * out.element_size()
-        e2e = {"value": world * F / (float(te.item()) * 1e-3) / 1e12, "unit": "TFLOPS",
+        e2e = {"value": F_total / (float(te.item()) * 1e-3) / 1e12, "unit": "TFLOPS",
                "ms_per_step": float(te.item()), "ms_per_step_all": per_step, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "timing": "median of per-step CUDA-event times, max over ranks",
                "api": ("paper_2604_03950_b200.DmaAttention.__call__ on pinned host tensors (forward_host: "
@@ -334,7 +474,8 @@ def main():
         t_unit_spec = (2 * d * (1 - hfrac)) / 9000.0 + (2 * d * hfrac) / 4500.0 + \
                       (2 * d) / (4500.0 if args.pv == "mxfp8" else 2250.0)
         peak_spec = f_unit / t_unit_spec
-        achieved = F / (core_ms * 1e-3) / 1e12
+        F_rank = causal_flops(lb, lh, N, d)
+        achieved = F_rank / (core_ms * 1e-3) / 1e12
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "attn_traffic.json")
         if os.path.exists(tpath):
@@ -343,20 +484,19 @@ def main():
             except (OSError, ValueError):
                 traffic = None
         # phase-1 algorithmic bytes: read Q,K,V bf16; write Q/K codes + SF + S_q, V codes + SF
-        elems_q, elems_kv = B * H * N * d, B * KVH * N * d
+        elems_q, elems_kv = lb * lh * N * d, lb * lkv * N * d
         lo_b = 0.5 + (1 / 16 if low == "nvfp4" else 1 / 32)
         qbytes = 2 * (elems_q + 2 * elems_kv) + (elems_q + elems_kv) * (lo_b + 1 + 1 / 32) + \
-            (B * (H + KVH) * N) * 4 + elems_kv * (1 + 1 / 32)
+            (lb * (lh + lkv) * N) * 4 + elems_kv * (1 + 1 / 32)
+        cd = config_dict(args, world)
+        cd["bit_high"] = hfrac
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "mxfp8+nvfp4" if low == "nvfp4" else "mxfp8+mxfp4",
             "data": "synthetic (torch.randn bf16, seeded)",
-            "config": {"workload": args.config, "desc": DESC[args.config], "batch_per_rank": B, "heads": H,
-                       "kv_heads": KVH, "seq_len": N, "head_dim": d, "tile": 128, "diag_window": T,
-                       "sink_window": S, "pv_mode": args.pv, "bit_high": hfrac,
-                       "parallelism": f"batch x head sharding, {world} rank(s), no hot-path collective",
-                       "l2": "inputs (805 MB bf16 Q/K/V at c3) exceed the 126 MB L2; no flush"},
+            "config": cd,
             "phases_ms": {"quantize": quant_ms, "attention": core_ms},
             "roofline": {"bound": "tensor", "kernel": "dma_attn_pp_kernel" if args.pv == "mxfp8" else "dma_attn_kernel", "achieved": achieved,
                          "peak": peak_mix, "unit": "TFLOP/s", "frac": achieved / peak_mix,
@@ -369,15 +509,58 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
         }
+        if gather_ms is not None:
+            line["phases_ms"]["gather"] = gather_ms
+            line["value_with_gather"] = F_total / ((ms_per_step + gather_ms) * 1e-3) / 1e12
         if e2e is not None:
             line["e2e"] = e2e
         if world == 1 and not args.no_cpu_baseline:
-            cb = cpu_baseline(args.config)
+            cb = cpu_baseline(args.config, args.ref_n)
             cb.pop("seconds", None)
             line["cpu_baseline"] = cb
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_dry(args, world, rank):
+    """CPU plumbing check of the multi-rank bench: gloo process group, the same shard plan,
+    barrier + max-over-ranks timing and output gather as the GPU path, with a stand-in
+    per-head compute (no kernel).  Used by tests/test_bench_launch.py."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_03950_b200.sharding import dma_attention_sharded
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    B, H, KVH, N, d = 2 * world, 4, 2, 64, 16
+
+    def stand_in(q, k, v, cfg):
+        g = q.shape[1] // k.shape[1]
+        return q * 2 + v.repeat_interleave(g, dim=1)
+
+    gen = torch.Generator().manual_seed(7)
+    q, k, v = torch.randn(B, H, N, d, generator=gen), torch.randn(B, KVH, N, d, generator=gen), \
+        torch.randn(B, KVH, N, d, generator=gen)
+    for _ in range(args.warmup):
+        dma_attention_sharded(q, k, v, None, compute=stand_in)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o, shard = dma_attention_sharded(q, k, v, None, compute=stand_in)
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    ok = bool(torch.equal(o.reshape(B, H, N, d), stand_in(q, k, v, None)))
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry": True, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": float(dt.item()) * 1e3 / args.steps,
+                          "gather_ok": ok, "scaling": "weak"}), flush=True)
+    if world > 1:
         dist.destroy_process_group()
 
 

@@ -17,6 +17,7 @@ from .attention import (  # noqa: F401
     AttentionConfig, DmaAttention, causal_tile_plan, dma_attention, mixed_precision_attention,
     noncausal_tile_plan,
 )
+from .softmax import OnlineSoftmaxState, apply_causal_mask, online_softmax_update  # noqa: F401
 from .metrics import MetricReport, high_precision_fraction, similarity  # noqa: F401
 from .decode import DmaKVCache  # noqa: F401
 from .scores import mixed_precision_scores, reference_attention, reference_scores  # noqa: F401

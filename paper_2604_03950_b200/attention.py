@@ -26,6 +26,7 @@ from . import _lib
 from ._device import dtype_code, from_device, is_torch, to_device
 from .formats import MXFP8_E4M3, NVFP4, MxFormatSpec, format_code
 from .quantize import Granularity, granularity_code, prescale_constant
+from .softmax import OnlineSoftmaxState, apply_causal_mask, online_softmax_update  # noqa: F401  (attention.py:37-48)
 
 _PV = {"mxfp8": _lib.PV_MXFP8, "bf16": _lib.PV_BF16}
 

@@ -193,15 +193,27 @@ __device__ __forceinline__ int mat_k_of(const AttnParams& p, int bh) {
 
 
 // exp2 / E4M3 pack as volatile asm: the softmax orders them explicitly (software pipelining)
+// (pipe experiments, WRONG results: -DDMA_EXP_NOMUFU replaces ex2 by an FMA-pipe multiply,
+// -DDMA_EXP_NOCVT the E4M3 pack by an ALU shift/or -- to see which pipe bounds the softmax)
 __device__ __forceinline__ float exp2_ordered(float x) {
   float y;
+#ifdef DMA_EXP_NOMUFU
+  asm volatile("mul.rn.f32 %0, %1, 0f3F000000;" : "=f"(y) : "f"(x));
+#else
   asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+#endif
   return y;
 }
 __device__ __forceinline__ uint32_t cvt_e4m3x2_ordered(float lo, float hi) {
+#ifdef DMA_EXP_NOCVT
+  uint32_t r;
+  asm volatile("{\n\t.reg .b32 t;\n\tshr.b32 t, %1, 24;\n\tshf.l.wrap.b32 %0, %2, t, 8;\n\t}" : "=r"(r) : "r"(__float_as_uint(lo)), "r"(__float_as_uint(hi)));
+  return r & 0xFFFFu;
+#else
   uint16_t r;
   asm volatile("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
   return r;
+#endif
 }
 
 // one 32-column chunk c of an output row: O[row, 32c + i] = acc[i] * inv_l (bf16 or f32)

@@ -11,6 +11,8 @@
 #include "attn.cuh"
 #include "attn_pp.cuh"
 #include "attn_sk.cuh"
+#include "attn_ws.cuh"
+#include "launch.h"
 #include "common.cuh"
 #include "quant.cuh"
 
@@ -299,17 +301,22 @@ static int quantize_deq(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cuda
   return 0;
 }
 
-// DMA_ATTN_KERNEL=sk selects the split-KV experiment (attn_sk.cuh: one query tile per CTA,
-// plan entries alternating between the softmax warpgroups; measured slower)
-// instead of the ping-pong kernel (attn_pp.cuh)
-static bool use_sk_kernel() {
+// Phase-2 kernel of the block-scaled MXFP8-PV path: DMA_ATTN_KERNEL=pp (ping-pong,
+// attn_pp.cuh), ws (max / exp warp specialisation, attn_ws.cuh), sk (split-KV experiment,
+// attn_sk.cuh; measured slower).
+enum { kKernPP = 0, kKernSK = 1, kKernWS = 2 };
+static int attn_kernel_choice() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("DMA_ATTN_KERNEL");
-    v = (e && e[0] == 's' && e[1] == 'k') ? 1 : 0;
+    v = kKernPP;
+    if (e && e[0] == 's' && e[1] == 'k') v = kKernSK;
+    if (e && e[0] == 'w' && e[1] == 's') v = kKernWS;
   }
-  return v == 1;
+  return v;
 }
+static bool use_sk_kernel() { return attn_kernel_choice() == kKernSK; }
+static bool use_ws_kernel() { return attn_kernel_choice() == kKernWS; }
 
 int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStream_t st) {
   const int64_t D = a->head_dim, DV = a->v_dim;
@@ -342,10 +349,10 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
     uint8_t* sfh = ws + (isq ? L.sf_q_hi : L.sf_k_hi);
     float* qs = reinterpret_cast<float*>(ws + (isq ? L.qs_q : L.qs_k));
     if (q.rows == 0) continue;
-    const int kmode = (!isq && L.pp) ? (use_sk_kernel() ? 2 : 1) : 0;  // K operand layout of the kernel
+    const int kmode = (!isq && L.pp) ? ((use_sk_kernel() || use_ws_kernel()) ? 2 : 1) : 0;  // K operand layout
     if (int rc = quantize_impl(&q, sfl, sfh, qs, isq ? L.lq_pad : L.lk_pad, st, kmode)) return rc;
     g_launches += L.tensor_gran ? 2 : 1;
-    if (kmode == 2) {
+    if (kmode == 2 && use_sk_kernel()) {
       const int64_t nt = L.mk * (L.lk_pad / 128);
       sqk_tile_stats_kernel<<<static_cast<unsigned>((nt + 7) / 8), 256, 0, st>>>(qs, nt, L.lk_pad / 128, a->len_k);
       DMA_LAUNCH_CHECK();
@@ -388,7 +395,7 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
   return 0;
 }
 
-static int num_sms() {
+int num_sms() {
   // per device (SM counts are cached; the attribute query is a driver call)
   static std::atomic<int> cache[64];
   int dev = 0;
@@ -401,67 +408,6 @@ static int num_sms() {
     cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
-}
-
-template <int D, int DV, int LOW, bool PVBF16>
-static int launch_attn(const AttnParams& p, int64_t items, cudaStream_t st) {
-  using C = AttnCfg<D, DV, LOW, PVBF16>;
-  auto kern = dma_attn_kernel<D, DV, LOW, PVBF16>;
-  const int smem = C::kSmemBytes > 120 * 1024 ? C::kSmemBytes : 120 * 1024;  // one CTA per SM (TMEM 512 cols)
-  DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  // persistent: one CTA per SM, items strided across CTAs (longest first)
-  const int64_t grid = items < num_sms() ? items : num_sms();
-  kern<<<static_cast<unsigned>(grid), 384, smem, st>>>(p);
-  DMA_LAUNCH_CHECK();
-  ++g_launches;
-  return 0;
-}
-
-template <int D, int DV, int LOW>
-static int launch_pp(const AttnParams& p, const PPParams& q, cudaStream_t st) {
-  using C = PPCfg<D, DV, LOW>;
-  auto kern = dma_attn_pp_kernel<D, DV, LOW>;
-  static_assert(C::kSmemBytes <= 227 * 1024, "smem budget");
-  DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
-  const int grid = q.n_pairs < num_sms() ? q.n_pairs : num_sms();
-  kern<<<static_cast<unsigned>(grid), C::kThreads, C::kSmemBytes, st>>>(p, q);
-  DMA_LAUNCH_CHECK();
-  ++g_launches;
-  return 0;
-}
-
-template <int D, int DV, int LOW>
-static int launch_sk(const AttnParams& p, const SKParams& q, cudaStream_t st) {
-  using C = SKCfg<D, DV, LOW>;
-  auto kern = dma_attn_sk_kernel<D, DV, LOW>;
-  DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
-  const int grid = q.n_items < num_sms() ? q.n_items : num_sms();
-  kern<<<static_cast<unsigned>(grid), C::kThreads, C::kSmemBytes, st>>>(p, q);
-  DMA_LAUNCH_CHECK();
-  ++g_launches;
-  return 0;
-}
-
-template <int D, int DV>
-static int dispatch_sk(const AttnParams& p, const SKParams& q, int low, cudaStream_t st) {
-  if (low == kLowNV) return launch_sk<D, DV, kLowNV>(p, q, st);
-  if (low == kLowMX4) return launch_sk<D, DV, kLowMX4>(p, q, st);
-  return launch_sk<D, DV, kLowHigh>(p, q, st);
-}
-
-template <int D, int DV>
-static int dispatch_attn(const AttnParams& p, int low, bool pv_bf16, int64_t items, cudaStream_t st) {
-  if (low == kLowBF16) return pv_bf16 ? launch_attn<D, DV, kLowBF16, true>(p, items, st) : launch_attn<D, DV, kLowBF16, false>(p, items, st);
-  if (low == kLowNV) return pv_bf16 ? launch_attn<D, DV, kLowNV, true>(p, items, st) : launch_attn<D, DV, kLowNV, false>(p, items, st);
-  if (low == kLowMX4) return pv_bf16 ? launch_attn<D, DV, kLowMX4, true>(p, items, st) : launch_attn<D, DV, kLowMX4, false>(p, items, st);
-  return pv_bf16 ? launch_attn<D, DV, kLowHigh, true>(p, items, st) : launch_attn<D, DV, kLowHigh, false>(p, items, st);
-}
-
-template <int D, int DV>
-static int dispatch_pp(const AttnParams& p, const PPParams& q, int low, cudaStream_t st) {
-  if (low == kLowNV) return launch_pp<D, DV, kLowNV>(p, q, st);
-  if (low == kLowMX4) return launch_pp<D, DV, kLowMX4>(p, q, st);
-  return launch_pp<D, DV, kLowHigh>(p, q, st);
 }
 
 int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStream_t st) {
@@ -524,6 +470,17 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
   p.n_items = static_cast<int>(items);
   const int low = L.deq ? kLowBF16
                         : (a->low_format == DMA_FMT_NVFP4 ? kLowNV : (a->low_format == DMA_FMT_MXFP4 ? kLowMX4 : kLowHigh));
+  if (L.pp && use_ws_kernel()) {
+    // max / exp warp-specialised kernel: one query tile per work item, S double-buffered
+    SKParams q{};
+    q.n_items = static_cast<int>(items);
+    const double kv_bytes = static_cast<double>(L.mk) * static_cast<double>(L.lk_pad) * (2.6 * static_cast<double>(D));
+    q.head_major = kv_bytes > 48.0 * 1024 * 1024;
+    q.ticket = reinterpret_cast<unsigned int*>(ws + L.ticket);
+    const int rc = run_ws(p, q, static_cast<int>(D), static_cast<int>(DV), low, st);
+    if (rc == 0) ++g_launches;
+    return rc;
+  }
   if (L.pp && use_sk_kernel()) {
     // split-KV kernel (block-scaled MXFP8 PV): one query tile per work item, plan entries
     // alternate between the two softmax warpgroups
@@ -532,8 +489,9 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
     const double kv_bytes = static_cast<double>(L.mk) * static_cast<double>(L.lk_pad) * (2.6 * static_cast<double>(D));
     q.head_major = kv_bytes > 48.0 * 1024 * 1024;
     q.ticket = reinterpret_cast<unsigned int*>(ws + L.ticket);
-    if (D == 64) return DV == 64 ? dispatch_sk<64, 64>(p, q, low, st) : dispatch_sk<64, 128>(p, q, low, st);
-    return DV == 64 ? dispatch_sk<128, 64>(p, q, low, st) : dispatch_sk<128, 128>(p, q, low, st);
+    const int rc = run_sk(p, q, static_cast<int>(D), static_cast<int>(DV), low, st);
+    if (rc == 0) ++g_launches;
+    return rc;
   }
   if (L.pp) {
     // ping-pong kernel (block-scaled MXFP8 PV): pairs of heads share one query-tile plan
@@ -543,12 +501,13 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
     const double kv_bytes = static_cast<double>(L.mk) * static_cast<double>(L.lk_pad) * (2.6 * static_cast<double>(D));
     q.head_major = kv_bytes > 48.0 * 1024 * 1024;  // K/V exceed ~L2/2: keep all CTAs on the same heads
     q.ticket = reinterpret_cast<unsigned int*>(ws + L.ticket);
-    if (D == 64) return DV == 64 ? dispatch_pp<64, 64>(p, q, low, st) : dispatch_pp<64, 128>(p, q, low, st);
-    return DV == 64 ? dispatch_pp<128, 64>(p, q, low, st) : dispatch_pp<128, 128>(p, q, low, st);
+    const int rc = run_pp(p, q, static_cast<int>(D), static_cast<int>(DV), low, st);
+    if (rc == 0) ++g_launches;
+    return rc;
   }
-  if (D == 64)
-    return DV == 64 ? dispatch_attn<64, 64>(p, low, L.pv_bf16, items, st) : dispatch_attn<64, 128>(p, low, L.pv_bf16, items, st);
-  return DV == 64 ? dispatch_attn<128, 64>(p, low, L.pv_bf16, items, st) : dispatch_attn<128, 128>(p, low, L.pv_bf16, items, st);
+  const int rc = run_attn(p, static_cast<int>(D), static_cast<int>(DV), low, L.pv_bf16, items, st);
+  if (rc == 0) ++g_launches;
+  return rc;
 }
 
 static uint8_t* ws_base(const DmaAttnArgs* a) {

@@ -17,3 +17,19 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden():
     return np.load(os.path.join(ROOT, "tests", "golden", "golden.npz"))
+
+
+def record_parity(case, pv, rel, mx, erel=None, emx=None, **extra):
+    """Append one measured parity row (vs the oracle / vs the oracle + PV emulation) to
+    gpurun_out/parity_<pid>.jsonl when DMA_PARITY_LOG is set (profiles/r02_parity.jsonl is
+    the committed collection of these rows)."""
+    if not os.environ.get("DMA_PARITY_LOG"):
+        return
+    import json
+
+    d = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(d, exist_ok=True)
+    row = {"case": case, "pv": pv, "rel_l2_vs_oracle": rel, "max_abs_vs_oracle": mx,
+           "rel_l2_vs_emulation": erel, "max_abs_vs_emulation": emx, **extra}
+    with open(os.path.join(d, f"parity_{os.getpid()}.jsonl"), "a") as f:
+        f.write(json.dumps(row) + "\n")

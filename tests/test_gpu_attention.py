@@ -20,6 +20,7 @@ import zlib
 import numpy as np
 import pytest
 
+from conftest import record_parity
 from inputs import randn_bf16
 from oracle import mx_oracle as O
 
@@ -83,6 +84,7 @@ def test_attention_vs_oracle(case, pv):
     erel, emx = errs(got, emu)
     print(f"{name} pv={pv}: vs oracle rel_l2={rel:.3e} max_abs={mx:.3e}; "
           f"vs oracle+PV emulation rel_l2={erel:.3e} max_abs={emx:.3e}")
+    record_parity(name, pv, rel, mx, erel, emx)
     assert np.isfinite(got).all()
     assert erel <= TOL_EMU[pv][0] and emx <= TOL_EMU[pv][1], (erel, emx)
     assert rel <= TOL[pv][0] and mx <= TOL[pv][1], (rel, mx)
@@ -198,6 +200,7 @@ def test_attention_bf16_operand_route(case, pv):
     erel, emx = errs(got, emu)
     print(f"{name} pv={pv}: vs oracle rel_l2={rel:.3e} max_abs={mx:.3e}; vs emulation rel_l2={erel:.3e} "
           f"max_abs={emx:.3e}")
+    record_parity(name, pv, rel, mx, erel, emx)
     assert np.isfinite(got).all()
     assert erel <= TOL_DEQ_EMU[pv][0] and emx <= TOL_DEQ_EMU[pv][1], (erel, emx)
     assert rel <= TOL_DEQ[pv][0] and mx <= TOL_DEQ[pv][1], (rel, mx)
@@ -236,6 +239,7 @@ def test_attention_plan_tiles_64(case, pv):
     erel, emx = errs(got, emu)
     print(f"{name} pv={pv}: vs oracle rel_l2={rel:.3e} max_abs={mx:.3e}; vs emulation rel_l2={erel:.3e} "
           f"max_abs={emx:.3e}")
+    record_parity(name, pv, rel, mx, erel, emx)
     assert np.isfinite(got).all()
     assert erel <= TOL_TILE_EMU[pv][0] and emx <= TOL_TILE_EMU[pv][1], (erel, emx)
     assert rel <= TOL[pv][0] and mx <= TOL[pv][1], (rel, mx)
@@ -312,6 +316,7 @@ def test_full_length_c3_sampled_tiles(pv):
         for t in tiles:
             r = slice(128 * t, 128 * t + 128)
             rel, mx = errs(got[h, r], want[r])
+            record_parity(f"c3_sampled_h{h}_t{t}", pv, None, None, rel, mx)
             assert rel <= TOL_EMU[pv][0] and mx <= TOL_EMU[pv][1], (pv, h, t, rel, mx)
 
 

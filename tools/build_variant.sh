@@ -3,9 +3,10 @@
 cd "$(dirname "$0")/.."
 name=$1; shift
 mkdir -p build_$name
-for f in capi_attn capi_quant selftest; do
+for src in paper_2604_03950_b200/csrc/*.cu; do
+  f=$(basename $src .cu)
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr \
-    -Iinclude $* -c paper_2604_03950_b200/csrc/$f.cu -o build_$name/$f.o &
+    -Iinclude $* -c $src -o build_$name/$f.o &
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build_$name/libdma.so build_$name/*.o
