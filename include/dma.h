@@ -208,6 +208,10 @@ const char* dma_last_error(void);
 int dma_abi_version(void);
 /* number of kernels launched by the last dma_attention_fwd on this thread */
 int dma_last_launch_count(void);
+/* Selects the fused forward for dma_attention_fwd (phase 1 inside the attention kernel, one
+ * kernel per call; bf16 inputs, TOKEN granularity, block-scaled PV): 1 on, 0 off (default,
+ * the two-phase path is faster on B200).  Returns the previous setting. */
+int dma_attention_set_fused(int on);
 
 #ifdef __cplusplus
 }

@@ -103,6 +103,8 @@ def lib():
         L.dma_last_error.restype = C.c_char_p
         L.dma_abi_version.restype = C.c_int
         L.dma_last_launch_count.restype = C.c_int
+        L.dma_attention_set_fused.restype = C.c_int
+        L.dma_attention_set_fused.argtypes = [C.c_int]
         L.dma_quantize_workspace_bytes.restype = sz
         L.dma_quantize_workspace_bytes.argtypes = [C.POINTER(DmaQuantArgs)]
         L.dma_quantize_dual.argtypes = [C.POINTER(DmaQuantArgs), vp]
@@ -146,7 +148,7 @@ EXPORTED_SYMBOLS = (
     "dma_encode_fp8", "dma_attention_workspace_bytes", "dma_attention_supported", "dma_attention_fwd",
     "dma_attention_quantize", "dma_attention_core", "dma_tile_plan", "dma_high_precision_fraction",
     "dma_selftest_mma", "dma_last_error", "dma_abi_version", "dma_last_launch_count",
-    "dma_decode_workspace_bytes", "dma_decode_attention",
+    "dma_decode_workspace_bytes", "dma_decode_attention", "dma_attention_set_fused",
 )
 
 

@@ -32,6 +32,7 @@
 #include "attn.cuh"
 #include "common.cuh"
 #include "ptx.cuh"
+#include "quant.cuh"
 
 namespace dma {
 
@@ -126,6 +127,89 @@ struct PPParams {
   int head_major;
   unsigned int* ticket;  // [0] next pair, [1] CTAs done (self-resetting)
 };
+
+// Fused phase 1 (FUSE instantiations, bf16 inputs, TOKEN granularity): warps 10 / 11 of
+// every CTA quantize K + V tiles / Q tiles of the raw inputs into the operand layouts
+// (the same q16_item / qv4_block code as quant16_kernel / quant_v4_bf16_kernel, so the codes
+// are bit-identical), in the order the attention consumes them, and publish each 128-row
+// tile with a ready flag (generic stores -> fence.proxy.async.global -> release store); the
+// TMA producer acquires the flag before it loads the tile.  Flags and counters live in the
+// workspace's small region, zeroed by the per-call memset.
+struct FuseParams {
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* k;
+  const __nv_bfloat16* v;
+  QuantOut out_q, out_k;     // as phase 1 (K: permuted operand rows, key_perm = 1)
+  uint8_t* v_codes;          // [mk][lk_pad][DV] E4M3
+  uint8_t* sf_v;             // V scale-factor atoms
+  double c;                  // softmax prescale log2(e) / sqrt(D) (quantize.py:92-95)
+  unsigned int* flags;       // [mq * rt_q] Q | [mk * rt_k] K | [mk * rt_k] V tile ready (0 / 1)
+  unsigned int* counters;    // [0] next K/V item, [1] next Q item
+  int e5;                    // high format E5M2
+};
+
+__device__ __forceinline__ void fuse_publish(unsigned int* flag, int lane) {
+  ptx::fence_proxy_async_global();  // this lane's generic stores -> visible to the async proxy (TMA)
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(1u) : "memory");
+  }
+}
+
+// One 128-row tile of bf16 Q or K quantized by one warp (fused kernel): tpr = D / 16 lanes per
+// row (q16_item_fast), 32 / tpr rows per pass, input bytes prefetched four passes ahead.  Out
+// of line: one copy of the quantizer code next to the attention code (instruction cache).
+template <int D, bool NV, bool E5>
+__device__ __noinline__ void fuse_quant_tile(const __nv_bfloat16* __restrict__ x, int64_t rows, int64_t mat, int t,
+                                             int is_query, double c, const QuantOut& out, int lane) {
+  constexpr int tpr = D / 16, rpp = 32 / tpr;
+  const int part = lane & (tpr - 1), rsub = lane / tpr;
+  const int64_t mstride = rows * D;
+  constexpr int kPasses = 128 / rpp, kPf = 4;
+  uint4 pf[kPf][2];
+  auto fetch = [&](int ps, uint4 (&dst)[2]) {
+    const int64_t r = static_cast<int64_t>(t) * 128 + ps * rpp + rsub;
+    if (ps < kPasses && r < rows) {
+      const uint4* src = reinterpret_cast<const uint4*>(x + mat * mstride + r * D + part * 16);
+      dst[0] = __ldg(src);
+      dst[1] = __ldg(src + 1);
+    } else {
+      dst[0] = dst[1] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < kPf; ++i) fetch(i, pf[i]);
+  for (int p0 = 0; p0 < kPasses; p0 += kPf) {
+#pragma unroll
+    for (int i = 0; i < kPf; ++i) {
+      const int ps = p0 + i;
+      const uint4 cur0 = pf[i][0], cur1 = pf[i][1];
+      fetch(ps + kPf, pf[i]);
+      const int64_t row = static_cast<int64_t>(t) * 128 + ps * rpp + rsub;
+      const bool live = row < rows;
+      if (!__all_sync(0xffffffffu, !live))
+        q16_item_fast<__nv_bfloat16, NV, E5, DMA_GRAN_TOKEN>(x, mstride, D, mat, rows, D, row, live, part, tpr, lane,
+                                                              cur0, cur1, is_query, c, nullptr, out);
+    }
+  }
+}
+
+__device__ __forceinline__ float ld_acquire_f32(const float* ptr) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return __uint_as_float(v);
+}
+
+__device__ __forceinline__ void fuse_acquire(const unsigned int* flag) {
+  uint32_t v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v) break;
+    __nanosleep(64);
+  }
+  ptx::fence_proxy_async_global();
+}
 
 template <int D, int DV, int LOW>
 struct PPCfg {
@@ -242,9 +326,10 @@ __device__ __forceinline__ void store_orow(const AttnParams& p, int64_t orow, in
   }
 }
 
-template <int D, int DV, int LOW>
+template <int D, int DV, int LOW, bool FUSE>
 __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_kernel(const __grid_constant__ AttnParams p,
-                                                             const __grid_constant__ PPParams pp) {
+                                                             const __grid_constant__ PPParams pp,
+                                                             const __grid_constant__ FuseParams fz) {
   using C = PPCfg<D, DV, LOW>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);  // keeps the shared address space
@@ -316,8 +401,10 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
   const uint32_t tmem = *tmem_slot;
 
   if (warp >= C::kSoftWarps) {
-  // register budget: the last warpgroup gives registers to the softmax warpgroups
-  ptx::setmaxnreg_dec<C::kRegCtl>();
+  // register budget: the last warpgroup gives registers to the softmax warpgroups (not when
+  // warps 10 / 11 quantize: the quantizer needs its registers; ptxas compiles every role at
+  // the launch bound anyway)
+  if (!FUSE) ptx::setmaxnreg_dec<C::kRegCtl>();
   // Producer and MMA issuer run as whole warps in lock-step (warp-uniform control
   // flow) and issue their async ops through ptx::wu: one elected lane, operands in
   // uniform registers, one SASS instruction per TMA / tcgen05 op.
@@ -358,6 +445,8 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       ++po;
       uint32_t qbytes = C::kQHiBytes + 512 * C::kChHi;
       if (LOW != kLowHigh) qbytes += C::kQLoBytes + 512 * C::kChLo;
+      if (FUSE)
+        for (int x = 0; x < ns; ++x) fuse_acquire(fz.flags + static_cast<int64_t>(bh[x]) * rt_q + qt);
       ptx::wu::mbar_arrive_expect_tx(q_full + qs, qbytes * ns);
       for (int x = 0; x < ns; ++x) {
         uint8_t* qdst = smem + C::oQ + (qs * 2 + x) * C::kQStream;
@@ -388,6 +477,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
           // S_q^K for the stream(s) reading this K tile
           const int s0 = x, s1 = shared_kv ? ns : x + 1;
           for (int y = s0; y < s1; ++y) ptx::mbar_wait(sq_empty + y * C::kNS + sqs[y], sqph[y] ^ 1);
+          if (FUSE) fuse_acquire(fz.flags + static_cast<int64_t>(p.n_bh) * rt_q + static_cast<int64_t>(mk[x]) * rt_k + t);
           PROF_MARK(4);
           ptx::wu::mbar_arrive_expect_tx(k_full + ks, kbytes + 512 * ch + C::kSqkBytes * (s1 - s0));
           ptx::wu::tma_load_3d(smem + C::oK + ks * C::kKBytes, hi ? &p.tm_k_hi : &p.tm_k_lo, k_full + ks, 0,
@@ -406,6 +496,9 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         for (int x = 0; x < nk; ++x) {
           PROF_MARK(0);
           ptx::mbar_wait(v_empty + vs, vph ^ 1);
+          if (FUSE)
+            fuse_acquire(fz.flags + static_cast<int64_t>(p.n_bh) * rt_q +
+                         static_cast<int64_t>(p.n_bh / p.group + mk[x]) * rt_k + t);
           PROF_MARK(5);
           ptx::wu::mbar_arrive_expect_tx(v_full + vs, C::kVBytes + 512);
           ptx::wu::tma_load_3d(smem + C::oV + vs * C::kVBytes, &p.tm_v, v_full + vs, 0, t * C::kBN, mk[x]);
@@ -613,6 +706,57 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
     }
     PROF_MARK(0);
     PROF_FLUSH(10, 10);
+  } else if (FUSE && (warp == kMma + 1 || warp == kMma + 2)) {
+    // =========================== fused phase 1: quantizer warps ===========================
+    // warp kMma + 1: K and V tiles, kv-head major (head-major pair order) or tile major;
+    // warp kMma + 2: Q tiles in the pair order.  One warp per 128-row tile: tpr = D / 16
+    // lanes per row (q16_item), 32 / tpr rows per pass, the next pass's 32 input bytes per
+    // lane prefetched while the current pass is quantized.
+    const int mq = p.n_bh, mkn = p.n_bh / p.group;
+    const bool kv_role = warp == kMma + 1;
+    const int64_t n_items = kv_role ? 2ll * mkn * rt_k : 2ll * pp.n_pairs;
+    auto quant_tile = [&](const __nv_bfloat16* x, int64_t rows, int64_t mat, int t, int is_query, const QuantOut& out) {
+      if (fz.e5)
+        fuse_quant_tile<D, LOW != kLowMX4, true>(x, rows, mat, t, is_query, fz.c, out, lane);
+      else
+        fuse_quant_tile<D, LOW != kLowMX4, false>(x, rows, mat, t, is_query, fz.c, out, lane);
+    };
+    for (;;) {
+      unsigned int it = 0;
+      if (lane == 0) it = atomicAdd(fz.counters + (kv_role ? 0 : 1), 1u);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (static_cast<int64_t>(it) >= n_items) break;
+      if (kv_role) {
+        const int kind = static_cast<int>(it & 1);  // 0 = K, 1 = V of the same tile
+        const int u = static_cast<int>(it >> 1);
+        int m, t;
+        if (pp.head_major) {
+          m = u / rt_k;
+          t = u - m * rt_k;
+        } else {
+          t = u / mkn;
+          m = u - t * mkn;
+        }
+        if (kind == 0) {
+          quant_tile(fz.k, p.lk, m, t, 0, fz.out_k);
+          fuse_publish(fz.flags + static_cast<int64_t>(mq) * rt_q + static_cast<int64_t>(m) * rt_k + t, lane);
+        } else {
+          // V: 4 key blocks of 32, DV / 4 lanes per block (qv4_block: 4 value columns per lane)
+          constexpr int tpb = DV / 4, bpp = 32 / tpb;
+          for (int kb = lane / tpb; kb < 4; kb += bpp)
+            qv4_block(fz.v, p.lk, DV, p.lk_pad, fz.v_codes, fz.sf_v, m, static_cast<int64_t>(t) * 4 + kb,
+                      (lane % tpb) * 4);
+          fuse_publish(fz.flags + static_cast<int64_t>(mq) * rt_q + static_cast<int64_t>(mkn + m) * rt_k + t, lane);
+        }
+      } else {
+        int bh[2], qt;
+        pair_coords(p, pp, static_cast<int>(it >> 1), bh[0], bh[1], qt);
+        const int b = bh[it & 1];
+        if (b < 0) continue;
+        quant_tile(fz.q, p.lq, b, qt, 1, fz.out_q);
+        fuse_publish(fz.flags + static_cast<int64_t>(b) * rt_q + qt, lane);
+      }
+    }
   } else if (kSplitPV && (warp == kMma + 1 || warp == kMma + 2)) {
     // =========================== PV issuers (kSplitPV): warp kMma + 1 + x issues stream x's PVs ===========================
     // PV_x(e) depends only on P_x(e) and V, so it must not queue behind QK_x(e + 1), which
@@ -668,7 +812,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
     }
   }
   } else {
-    ptx::setmaxnreg_inc<C::kRegSoft>();
+    if (!FUSE) ptx::setmaxnreg_inc<C::kRegSoft>();
     // =========================== softmax (kSplit warpgroups per stream) ===========================
     // TMEM is read in the 32x32b shape: thread = one query row (lane of its warp's
     // 32-lane sub-partition) and NK = 128 / kSplit S columns.  With kSplit = 2 the two
@@ -718,7 +862,9 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       const bool pair2 = bh[1] >= 0;
       const int q0 = qt * C::kBM;
       const int qrow = q0 + row;
-      const float sq_q = (qrow < p.lq) ? p.qs_q[static_cast<int64_t>(my_bh) * p.lq_pad + qrow] : 1.0f;
+      // S_q^Q of this row; in the fused kernel it is written by the quantizer warps, so it is
+      // read after the pair's first S is ready (which follows the producer's acquire of the Q flag)
+      float sq_q = (!FUSE && qrow < p.lq) ? p.qs_q[static_cast<int64_t>(my_bh) * p.lq_pad + qrow] : 1.0f;
       float m_run = -INFINITY;
       float2 l2 = make_float2(0.f, 0.f);
 
@@ -732,6 +878,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         PROF_MARK(9);
         ptx::mbar_wait(s_full + x, g & 1);
         ptx::tc_fence_after();
+        if (FUSE && e == 0 && qrow < p.lq) sq_q = ld_acquire_f32(p.qs_q + static_cast<int64_t>(my_bh) * p.lq_pad + qrow);
         TRACE(tw, x, 1);
         PROF_MARK(0);
         // load the first half of this thread's columns, start the second, scale the first while it lands

@@ -86,7 +86,7 @@ struct Layout {
   size_t r_pl[2], r_sl[2], r_hc[2], r_sh[2], r_qs[2];
   // byte offsets
   size_t q_hi, q_lo, k_hi, k_lo, v_codes, v_bf16;  // large buffers
-  size_t small_begin, sf_q_hi, sf_q_lo, sf_k_hi, sf_k_lo, sf_v, qs_q, qs_k, ticket, small_end;
+  size_t small_begin, sf_q_hi, sf_q_lo, sf_k_hi, sf_k_lo, sf_v, qs_q, qs_k, ticket, fuse_flags, small_end;
   size_t absmax_q, absmax_k, total;
 };
 
@@ -143,6 +143,8 @@ static Layout plan_layout(const DmaAttnArgs* a) {
   L.qs_q = take(L.mq * L.lq_pad * 4);
   L.qs_k = take(L.pp ? L.mk * (L.lk_pad / 128) * kSqkTile * 4 : L.mk * L.lk_pad * 4);
   L.ticket = take(64);  // dynamic pair scheduler ticket (zeroed with the small region; self-resetting)
+  // fused forward: per 128-row tile ready flags (Q, K, V) + the quantizer work counters
+  L.fuse_flags = L.pp ? take((L.mq * (L.lq_pad / 128) + 2 * L.mk * (L.lk_pad / 128)) * 4 + 64) : 0;
   L.small_end = off;
   L.absmax_q = L.tensor_gran ? take(L.mq * 8) : 0;
   L.absmax_k = L.tensor_gran ? take(L.mk * 8) : 0;
@@ -317,13 +319,32 @@ static int attn_kernel_choice() {
 }
 static bool use_sk_kernel() { return attn_kernel_choice() == kKernSK; }
 static bool use_ws_kernel() { return attn_kernel_choice() == kKernWS; }
+// The fused forward (phase 1 inside the ping-pong kernel, attn_pp.cuh FUSE) covers the
+// north-star path: bf16 inputs, TOKEN granularity, MX formats, block-scaled MXFP8 PV,
+// 128-tiles.  Its output is bit-identical to the two-phase path, but it is slower (DESIGN.md
+// §4.6: two quantizer warps per SM are latency-bound), so it is opt-in:
+// dma_attention_set_fused(1) or DMA_FUSE=1.
+static std::atomic<int> g_fuse{-1};
+static bool fuse_enabled() {
+  int v = g_fuse.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("DMA_FUSE");
+    v = (e && e[0] == '1') ? 1 : 0;
+    g_fuse.store(v, std::memory_order_relaxed);
+  }
+  return v == 1;
+}
+
+static bool fused_eligible(const DmaAttnArgs* a, const Layout& L) {
+  return fuse_enabled() && L.pp && !use_sk_kernel() && !use_ws_kernel() && a->in_dtype == DMA_DT_BF16 &&
+         a->granularity == DMA_GRAN_TOKEN && a->len_q > 0 && a->len_k > 0;
+}
 
 int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStream_t st) {
   const int64_t D = a->head_dim, DV = a->v_dim;
   const bool nv = a->low_format == DMA_FMT_NVFP4;
   // padded SF atoms / S_q entries must be finite: zero the small region once per call
-  DMA_CUDA_TRY(cudaMemsetAsync(ws + L.small_begin, 0, L.small_end - L.small_begin, st));
-  ++g_launches;
+  DMA_CUDA_TRY(cudaMemsetAsync(ws + L.small_begin, 0, L.small_end - L.small_begin, st));  // (a memset, not a kernel)
   if (a->nonfinite) DMA_CUDA_TRY(cudaMemsetAsync(a->nonfinite, 0, sizeof(uint32_t), st));
   for (int which = 0; which < 2 && !L.deq; ++which) {
     const bool isq = which == 0;
@@ -410,7 +431,7 @@ int num_sms() {
   return n;
 }
 
-int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStream_t st) {
+int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStream_t st, bool fuse = false) {
   const int64_t D = a->head_dim, DV = a->v_dim;
   AttnParams p;
   std::memset(&p, 0, sizeof(p));
@@ -501,7 +522,35 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
     const double kv_bytes = static_cast<double>(L.mk) * static_cast<double>(L.lk_pad) * (2.6 * static_cast<double>(D));
     q.head_major = kv_bytes > 48.0 * 1024 * 1024;  // K/V exceed ~L2/2: keep all CTAs on the same heads
     q.ticket = reinterpret_cast<unsigned int*>(ws + L.ticket);
-    const int rc = run_pp(p, q, static_cast<int>(D), static_cast<int>(DV), low, st);
+    int rc;
+    if (fuse) {
+      // phase 1 inside the kernel (attn_pp.cuh FuseParams): raw bf16 inputs, operand outputs as
+      // attention_quantize writes them
+      FuseParams fz{};
+      fz.q = static_cast<const __nv_bfloat16*>(a->q);
+      fz.k = static_cast<const __nv_bfloat16*>(a->k);
+      fz.v = static_cast<const __nv_bfloat16*>(a->v);
+      for (int w = 0; w < 2; ++w) {
+        QuantOut& o = w == 0 ? fz.out_q : fz.out_k;
+        o.packed_low = L.low_fp4 ? ws + (w == 0 ? L.q_lo : L.k_lo) : nullptr;
+        o.high_codes = ws + (w == 0 ? L.q_hi : L.k_hi);
+        o.sf_low_op = L.low_fp4 ? ws + (w == 0 ? L.sf_q_lo : L.sf_k_lo) : nullptr;
+        o.sf_high_op = ws + (w == 0 ? L.sf_q_hi : L.sf_k_hi);
+        o.qs_f32 = reinterpret_cast<float*>(ws + (w == 0 ? L.qs_q : L.qs_k));
+        o.nonfinite = a->nonfinite;
+        o.rows_pad = w == 0 ? L.lq_pad : L.lk_pad;
+        o.key_perm = w == 0 ? 0 : 1;
+      }
+      fz.v_codes = ws + L.v_codes;
+      fz.sf_v = ws + L.sf_v;
+      fz.c = a->prescale;
+      fz.flags = reinterpret_cast<unsigned int*>(ws + L.fuse_flags);
+      fz.counters = fz.flags + (L.mq * (L.lq_pad / 128) + 2 * L.mk * (L.lk_pad / 128));
+      fz.e5 = a->high_format == DMA_FMT_MXFP8_E5M2;
+      rc = run_pp_fused(p, q, fz, static_cast<int>(D), static_cast<int>(DV), low, st);
+    } else {
+      rc = run_pp(p, q, static_cast<int>(D), static_cast<int>(DV), low, st);
+    }
     if (rc == 0) ++g_launches;
     return rc;
   }
@@ -579,11 +628,24 @@ int dma_attention_fwd(const DmaAttnArgs* a, void* stream) {
                 a->workspace_bytes, L.total);
   DMA_CHECK_ARG(a->q && a->k && a->v && a->o, "null tensor pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (fused_eligible(a, L)) {
+    // one kernel: the ping-pong attention with phase 1 in warps 10 / 11 (attn_pp.cuh FUSE)
+    uint8_t* ws = ws_base(a);
+    DMA_CUDA_TRY(cudaMemsetAsync(ws + L.small_begin, 0, L.small_end - L.small_begin, st));
+    if (a->nonfinite) DMA_CUDA_TRY(cudaMemsetAsync(a->nonfinite, 0, sizeof(uint32_t), st));
+    return attention_core(a, L, ws, st, true);
+  }
   if (int rc = attention_quantize(a, L, ws_base(a), st)) return rc;
   return attention_core(a, L, ws_base(a), st);
 }
 
 int dma_last_launch_count(void) { return g_launches; }
+
+int dma_attention_set_fused(int on) {
+  const int prev = fuse_enabled() ? 1 : 0;
+  g_fuse.store(on ? 1 : 0, std::memory_order_relaxed);
+  return prev;
+}
 
 #ifdef DMA_TRACE
 // tracing builds only: copy out and clear the CTA-0 event trace ([6][4096] + counts)

@@ -1,0 +1,40 @@
+// Launch templates of the ping-pong kernel (attn_pp.cuh), instantiated by kern_pp.cu
+// (phase 2 only) and kern_ppf.cu (phase 1 fused in) -- two translation units so the
+// instantiations compile in parallel.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "attn_pp.cuh"
+#include "common.cuh"
+#include "launch.h"
+
+namespace dma {
+
+template <int D, int DV, int LOW, bool FUSE>
+static int launch_pp(const AttnParams& p, const PPParams& q, const FuseParams& fz, cudaStream_t st) {
+  using C = PPCfg<D, DV, LOW>;
+  auto kern = dma_attn_pp_kernel<D, DV, LOW, FUSE>;
+  static_assert(C::kSmemBytes <= 227 * 1024, "smem budget");
+  DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+  const int grid = q.n_pairs < num_sms() ? q.n_pairs : num_sms();
+  kern<<<static_cast<unsigned>(grid), C::kThreads, C::kSmemBytes, st>>>(p, q, fz);
+  DMA_LAUNCH_CHECK();
+  return 0;
+}
+
+template <int D, int DV, bool FUSE>
+static int dispatch_pp(const AttnParams& p, const PPParams& q, const FuseParams& fz, int low, cudaStream_t st) {
+  if (low == kLowNV) return launch_pp<D, DV, kLowNV, FUSE>(p, q, fz, st);
+  if (low == kLowMX4) return launch_pp<D, DV, kLowMX4, FUSE>(p, q, fz, st);
+  return launch_pp<D, DV, kLowHigh, FUSE>(p, q, fz, st);
+}
+
+template <bool FUSE>
+static int run_pp_t(const AttnParams& p, const PPParams& q, const FuseParams& fz, int D, int DV, int low,
+                    cudaStream_t st) {
+  if (D == 64) return DV == 64 ? dispatch_pp<64, 64, FUSE>(p, q, fz, low, st) : dispatch_pp<64, 128, FUSE>(p, q, fz, low, st);
+  return DV == 64 ? dispatch_pp<128, 64, FUSE>(p, q, fz, low, st) : dispatch_pp<128, 128, FUSE>(p, q, fz, low, st);
+}
+
+}  // namespace dma

@@ -340,51 +340,15 @@ __device__ __forceinline__ double shfl_max(double v, int lanes) {
   return v;
 }
 
+// One quantize_dual step of one thread: 16 consecutive columns (``part``) of one row of one
+// matrix (quantize.py:122-212), with the row's other tpr - 1 parts on the adjacent lanes.
+// bf16 inputs arrive as the 32 prefetched bytes cur0 / cur1, other types are loaded here.
+// Shared by quant16_kernel (phase 1) and the fused attention kernel (attn_pp.cuh).
 template <typename T, bool NV, bool E5, int GRAN>
-__global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, int64_t n_mat, int64_t rows,
-                                                      int cols, int64_t mat_stride, int64_t row_stride,
-                                                      int is_query, double c,
-                                                      const unsigned long long* __restrict__ tensor_absmax,
-                                                      QuantOut out) {
-  // Work item = (matrix, block of 256 / tpr rows); a CTA walks items grid-stride
-  // (x over row blocks, y over matrices) and prefetches the next item's 32 input bytes
-  // while it quantizes the current one (the kernel is latency-bound otherwise).
-  const int lg_tpr = __ffs(cols >> 4) - 1;  // tpr = cols / 16, a power of two in [2, 32]
-  const int tpr = 1 << lg_tpr;
-  const int lane = threadIdx.x & 31;
-  const int part = threadIdx.x & (tpr - 1);
-  const int rpb = 256 >> lg_tpr;  // rows per block
-  const int64_t nbx = (rows + rpb - 1) / rpb;
-  const int rsub = threadIdx.x >> lg_tpr;
-  uint4 pf0 = make_uint4(0u, 0u, 0u, 0u), pf1 = pf0;  // prefetched words (bf16 inputs)
-  auto fetch = [&](int64_t m, int64_t b) {
-    const int64_t r = b * rpb + rsub;
-    if constexpr (sizeof(T) == 2) {
-      if (m < n_mat && r < rows) {
-        const uint4* src = reinterpret_cast<const uint4*>(x + m * mat_stride + r * row_stride + part * 16);
-        pf0 = __ldg(src);
-        pf1 = __ldg(src + 1);
-      } else {
-        pf0 = pf1 = make_uint4(0u, 0u, 0u, 0u);
-      }
-    }
-  };
-  fetch(blockIdx.y, blockIdx.x);
-  for (int64_t mat = blockIdx.y; mat < n_mat; mat += gridDim.y) {
-  for (int64_t bx = blockIdx.x; bx < nbx; bx += gridDim.x) {
-  const int64_t row = bx * rpb + rsub;
-  const bool live = row < rows;  // whole rows live or die together (tpr | 32)
-  const uint4 cur0 = pf0, cur1 = pf1;
-  {
-    int64_t nb = bx + gridDim.x, nm = mat;
-    if (nb >= nbx) {
-      nb = blockIdx.x;
-      nm = mat + gridDim.y;
-    }
-    fetch(nm, nb);
-  }
-  if (__all_sync(0xffffffffu, !live)) continue;
-
+__device__ __forceinline__ void q16_item(const T* __restrict__ x, int64_t mat_stride, int64_t row_stride, int64_t mat,
+                                         int64_t rows, int cols, int64_t row, bool live, int part, int tpr, int lane,
+                                         uint4 cur0, uint4 cur1, int is_query, double c,
+                                         const unsigned long long* __restrict__ tensor_absmax, const QuantOut& out) {
   // Maxima use monotonicity instead of per-element f64 compares: fl(|x| c) and the
   // correctly rounded fl(|x| / S_q) are non-decreasing in |x|, so the max of the
   // rounded values is the rounded max (the argument quantize.py's TENSOR path
@@ -498,7 +462,7 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
     codes[j] = w;
   }
   const uint32_t sc_high = static_cast<uint32_t>(he + 127);
-  if (!live) continue;  // dead rows still take part in the next matrix's shuffles
+  if (!live) return;  // dead rows still take part in the shuffles above
 
   const int64_t rbase = mat * rows + row;
   // operand row of the codes / scale-factor atoms (permuted inside 128-row tiles for attn_pp)
@@ -537,6 +501,342 @@ __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, i
         out.qs_f32[mat * out.rows_pad + row] = static_cast<float>(sq);
     }
   }
+}
+
+// ------------------------------------------------------------------------
+// Fast variant of q16_item (the one phase 1 and the fused kernel use): the per-row /
+// per-block scale decisions stay exact float64 exactly as in q16_item, the per-element
+// work runs in float32:
+//   v_f = x * c * (1/S_q) [* (1/sv) | * 2^-e | * 2^-he]  (relative error < 8 * 2^-24
+//         against the float64 value v the reference rounds, for rows whose S_q and blocks
+//         whose max lie well inside the float32 range -- checked, else the float64 path);
+//   the code of v is the code of every point of [v_f (1 - 2^-20), v_f (1 + 2^-20)] when
+//   the two ends round to the same code (cvt RN is monotone), so the float32 codes are
+//   taken when cvt(lo) == cvt(hi) for all 16 values of the thread, and the thread redoes
+//   its 16 values in float64 (q16_item's arithmetic) otherwise -- near a rounding
+//   midpoint, ~2^-17 of the elements.  Bit-exact either way.
+// ------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void load16_f64(const T* __restrict__ x, int64_t off, uint4 cur0, uint4 cur1,
+                                           double (&xs)[16]) {
+  if constexpr (sizeof(T) == 2) {
+    const uint32_t w[8] = {cur0.x, cur0.y, cur0.z, cur0.w, cur1.x, cur1.y, cur1.z, cur1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      xs[2 * i] = __uint_as_float(w[i] << 16);
+      xs[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  } else {
+    Load16<T>::run(x + off, xs);
+  }
+}
+
+// float64 per-element codes of one thread's 16 values (q16_item's arithmetic), given the
+// row / block scale decisions: the fallback of q16_item_fast (rare; kept out of line so the
+// fast path's register allocation does not carry the float64 arrays)
+template <typename T, bool NV, bool E5>
+__device__ __noinline__ void q16_codes_f64(const T* __restrict__ x, int64_t off, uint4 cur0, uint4 cur1, bool live,
+                                           int is_query, double c, double sq, double ysq, double sv, double ysv,
+                                           double inv, double hinv, uint32_t (&packed)[2], uint32_t (&codes)[4]) {
+  double xs[16];
+  if (live) {
+    load16_f64<T>(x, off, cur0, cur1, xs);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) xs[i] = 0.0;
+  }
+  if (is_query) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) xs[i] = __dmul_rn(xs[i], c);  // quantize.py:149 (x * c)
+  }
+  double xsc[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) xsc[i] = qdiv<T>(xs[i], sq, ysq);  // quantize.py:154
+  packed[0] = packed[1] = 0u;
+#pragma unroll
+  for (int i = 0; i < 16; i += 2) {
+    double l0, l1;
+    if (NV) {
+      l0 = qdiv<T>(xsc[i], sv, ysv);
+      l1 = qdiv<T>(xsc[i + 1], sv, ysv);
+    } else {
+      l0 = xs[i] * inv;
+      l1 = xs[i + 1] * inv;
+    }
+    uint32_t b = ptx::cvt_e2m1x2(rto_abs(l0), rto_abs(l1));
+    b |= (neg_nonzero(l0) ? 0x08u : 0u) | (neg_nonzero(l1) ? 0x80u : 0u);
+    packed[i >> 3] |= b << (4 * (i & 7));
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i += 2) {
+      const double h0 = xsc[4 * j + i] * hinv, h1 = xsc[4 * j + i + 1] * hinv;
+      const float a = rto_abs(h0), b = rto_abs(h1);
+      const uint32_t mag = E5 ? ptx::cvt_e5m2x2(a, b) : ptx::cvt_e4m3x2(a, b);
+      uint32_t c0 = mag & 0xFF, c1 = (mag >> 8) & 0xFF;
+      if (c0 && neg_nonzero(h0)) c0 |= 0x80;  // rounded-to-zero magnitudes stay +0
+      if (c1 && neg_nonzero(h1)) c1 |= 0x80;
+      w |= (c0 | (c1 << 8)) << (8 * i);
+    }
+    codes[j] = w;
+  }
+}
+
+template <typename T, bool NV, bool E5, int GRAN>
+__device__ __forceinline__ void q16_item_fast(const T* __restrict__ x, int64_t mat_stride, int64_t row_stride,
+                                              int64_t mat, int64_t rows, int cols, int64_t row, bool live, int part,
+                                              int tpr, int lane, uint4 cur0, uint4 cur1, int is_query, double c,
+                                              const unsigned long long* __restrict__ tensor_absmax,
+                                              const QuantOut& out) {
+  const int64_t off = mat * mat_stride + row * row_stride + part * 16;
+  // ---- this thread's 16 inputs as float32 (exact for bf16 / f32) and max |x| (exact)
+  float xf[16];
+  double amax;
+  bool bad;
+  bool in_f32 = true;  // every input exactly representable in float32
+  if constexpr (sizeof(T) == 2) {
+    const uint32_t w[8] = {cur0.x, cur0.y, cur0.z, cur0.w, cur1.x, cur1.y, cur1.z, cur1.w};
+    uint32_t mm = w[0] & 0x7FFF7FFFu;
+#pragma unroll
+    for (int i = 1; i < 8; ++i) mm = __vmaxu2(mm, w[i] & 0x7FFF7FFFu);
+    const uint32_t m16 = max(mm & 0xFFFFu, mm >> 16);
+    bad = m16 >= 0x7F80u;
+    amax = static_cast<double>(__uint_as_float(m16 << 16));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      xf[2 * i] = __uint_as_float(w[i] << 16);
+      xf[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  } else {
+    double xs[16];
+    if (live) {
+      Load16<T>::run(x + off, xs);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) xs[i] = 0.0;
+    }
+    bad = false;
+    amax = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      bad |= (static_cast<uint32_t>(__double2hiint(xs[i])) & 0x7FF00000u) == 0x7FF00000u;  // Inf / NaN
+      amax = fmax(amax, fabs(xs[i]));
+      xf[i] = static_cast<float>(xs[i]);
+      if constexpr (sizeof(T) == 8) in_f32 &= static_cast<double>(xf[i]) == xs[i];
+    }
+  }
+  if (out.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(out.nonfinite, 1u);
+
+  // ---- scale decisions in float64, exactly as q16_item (quantize.py:98-106, 152-199)
+  double g;
+  if (GRAN == DMA_GRAN_TOKEN) {
+    g = shfl_max(amax, tpr);
+  } else if (GRAN == DMA_GRAN_BLOCK) {
+    g = shfl_max(amax, 2);
+  } else {
+    g = __longlong_as_double(static_cast<long long>(tensor_absmax[mat]));
+  }
+  if (is_query) {
+    amax = __dmul_rn(amax, c);
+    g = __dmul_rn(g, c);
+  }
+  const double sq = g > 0.0 ? __ddiv_rn(g, 2688.0) : 1.0;
+  const double ysq = __drcp_rn(sq);
+  const double amax_sc = qdiv<T>(amax, sq, ysq);
+  uint32_t sc_low;
+  double sv = 1.0, ysv = 1.0, inv = 1.0;
+  if (NV) {
+    const double bm = amax_sc;
+    uint32_t code = bm > 0.0 ? e4m3_pos(__ddiv_rn(bm, 6.0)) : 0x38u;
+    if (code == 0 && bm > 0.0) code = 0x01;  // floor at 2^-9 (quantize.py:164-167)
+    sv = decode_e4m3(code);
+    ysv = __drcp_rn(sv);
+    sc_low = code;
+  } else {
+    const double bm = shfl_max(amax, 2);  // 32-column block = 2 lanes, single level on x_sm
+    const int e = bm > 0.0 ? min(max(floor_log2_pos(bm) - 2, -127), 127) : -127;
+    inv = pow2(-e);
+    sc_low = static_cast<uint32_t>(e + 127);
+  }
+  const double hm = shfl_max(amax_sc, 2);
+  constexpr int kEmax = E5 ? 15 : 8;
+  const int he = hm > 0.0 ? min(max(floor_log2_pos(hm) - kEmax, -127), 127) : -127;
+  const double hinv = pow2(-he);
+  const uint32_t sc_high = static_cast<uint32_t>(he + 127);
+
+  // ---- float32 fast path (guards: every factor and this thread's |x| range well inside float32)
+  const double lfac = NV ? ysv : inv;
+  const bool guard = in_f32 && sq >= 0x1p-100 && sq <= 0x1p+100 && (amax == 0.0 || (amax >= 0x1p-100 && amax <= 0x1p+100)) &&
+                     lfac >= 0x1p-120 && lfac <= 0x1p+120 && hinv >= 0x1p-120 && hinv <= 0x1p+120;
+  uint32_t packed[2] = {0u, 0u}, codes[4] = {0u, 0u, 0u, 0u};
+  bool ok = guard;
+  uint32_t fl = 0u;  // elements whose float32 interval straddles a rounding boundary
+  if (guard) {
+    const float cf = is_query ? static_cast<float>(c) : 1.0f;
+    const float rsq = static_cast<float>(ysq);
+    const float lf = static_cast<float>(lfac), hf = static_cast<float>(hinv);
+    constexpr float kD = 0x1p-20f;
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+      // x_sm (Q: x * c), x_scaled = x_sm / S_q.  The +0 addend of the first step turns an
+      // input -0 into +0 (the reference's v < 0 tests see -0.0 as non-negative); later steps
+      // are plain products, so a negative value that underflows keeps its sign (-0), as the
+      // reference's negative nonzero float64 value does
+      const float2 xsm = __ffma2_rn(make_float2(xf[i], xf[i + 1]), make_float2(cf, cf), make_float2(0.f, 0.f));
+      const float2 xsc = __fmul2_rn(xsm, make_float2(rsq, rsq));
+      // 4-bit: NVFP4 x_scaled / sv, MXFP4 x_sm * 2^-e
+      const float2 l = NV ? __fmul2_rn(xsc, make_float2(lf, lf)) : __fmul2_rn(xsm, make_float2(lf, lf));
+      const float2 lhi = __ffma2_rn(l, make_float2(kD, kD), l), llo = __ffma2_rn(l, make_float2(-kD, -kD), l);
+      const uint32_t ma = ptx::cvt_e2m1x2(fabsf(lhi.x), fabsf(lhi.y)), mb = ptx::cvt_e2m1x2(fabsf(llo.x), fabsf(llo.y));
+      const uint32_t sg = ((__float_as_uint(l.x) >> 31) << 3) | ((__float_as_uint(l.y) >> 31) << 7);
+      packed[i >> 3] |= (ma | sg) << (4 * (i & 7));
+      // 8-bit: x_scaled * 2^-he
+      const float2 h = __fmul2_rn(xsc, make_float2(hf, hf));
+      const float2 hhi = __ffma2_rn(h, make_float2(kD, kD), h), hlo = __ffma2_rn(h, make_float2(-kD, -kD), h);
+      const uint32_t ha = E5 ? ptx::cvt_e5m2x2(fabsf(hhi.x), fabsf(hhi.y)) : ptx::cvt_e4m3x2(fabsf(hhi.x), fabsf(hhi.y));
+      const uint32_t hb = E5 ? ptx::cvt_e5m2x2(fabsf(hlo.x), fabsf(hlo.y)) : ptx::cvt_e4m3x2(fabsf(hlo.x), fabsf(hlo.y));
+      // sign on nonzero magnitudes only (rounded-to-zero magnitudes stay +0)
+      const uint32_t hs = ((__float_as_uint(h.x) >> 31) << 7) | ((__float_as_uint(h.y) >> 31) << 15);
+      const uint32_t hcode = ha | (hs & __vcmpne4(ha, 0u));
+      codes[i >> 2] |= (hcode & 0xFFFFu) << (8 * (i & 3));
+      const uint32_t d4 = ma ^ mb, d8 = ha ^ hb;
+      fl |= ((((d4 & 0x0Fu) | (d8 & 0x00FFu)) != 0u ? 1u : 0u) | (((d4 & 0xF0u) | (d8 & 0xFF00u)) != 0u ? 2u : 0u)) << i;
+    }
+  }
+  {
+    // the flagged elements (~1-2 per row: the row maximum lands exactly on an E4M3 midpoint
+    // after x / S_q = 2688) in float64, one per lane per round
+    while (__any_sync(0xffffffffu, fl != 0u)) {
+      if (fl) {
+        const int j = __ffs(fl) - 1;
+        fl &= fl - 1u;
+        double xj;
+        if constexpr (sizeof(T) == 2) {
+          const uint32_t w = (j >> 1) < 4 ? ((j >> 1) == 0 ? cur0.x : (j >> 1) == 1 ? cur0.y : (j >> 1) == 2 ? cur0.z : cur0.w)
+                                         : ((j >> 1) == 4 ? cur1.x : (j >> 1) == 5 ? cur1.y : (j >> 1) == 6 ? cur1.z : cur1.w);
+          xj = __uint_as_float((j & 1) ? (w & 0xFFFF0000u) : (w << 16));
+        } else {
+          xj = static_cast<double>(x[off + j]);
+        }
+        const double xs = is_query ? __dmul_rn(xj, c) : xj;  // quantize.py:149
+        const double xsc = qdiv<T>(xs, sq, ysq);               // quantize.py:154
+        const double lv = NV ? qdiv<T>(xsc, sv, ysv) : xs * inv;
+        const uint32_t lc = (ptx::cvt_e2m1x2(rto_abs(lv), 0.f) & 0xFu) | (neg_nonzero(lv) ? 0x8u : 0u);
+        const double hv = xsc * hinv;
+        const float ha = rto_abs(hv);
+        uint32_t hc = (E5 ? ptx::cvt_e5m2x2(ha, 0.f) : ptx::cvt_e4m3x2(ha, 0.f)) & 0xFFu;
+        if (hc && neg_nonzero(hv)) hc |= 0x80u;
+        const uint32_t s4 = 4u * (j & 7), s8 = 8u * (j & 3);
+        if (j < 8) packed[0] = (packed[0] & ~(0xFu << s4)) | (lc << s4);
+        else packed[1] = (packed[1] & ~(0xFu << s4)) | (lc << s4);
+        const int cw = j >> 2;
+        const uint32_t m8 = ~(0xFFu << s8), v8 = hc << s8;
+        codes[0] = cw == 0 ? ((codes[0] & m8) | v8) : codes[0];
+        codes[1] = cw == 1 ? ((codes[1] & m8) | v8) : codes[1];
+        codes[2] = cw == 2 ? ((codes[2] & m8) | v8) : codes[2];
+        codes[3] = cw == 3 ? ((codes[3] & m8) | v8) : codes[3];
+      }
+    }
+  }
+  if (!ok) q16_codes_f64<T, NV, E5>(x, off, cur0, cur1, live, is_query, c, sq, ysq, sv, ysv, inv, hinv, packed, codes);
+  if (!live) return;
+
+  // ---- stores (as q16_item)
+  const int64_t rbase = mat * rows + row;
+  const int64_t orow = out.key_perm == 1 ? ((row & ~int64_t(127)) | perm_row(static_cast<int>(row & 127))) : row;
+  const int64_t cbase = out.key_perm ? mat * out.rows_pad + orow : rbase;
+  const int col0 = part * 16;
+  if (out.packed_low)
+    *reinterpret_cast<uint2*>(out.packed_low + cbase * (cols / 2) + col0 / 2) = make_uint2(packed[0], packed[1]);
+  if (out.high_codes)
+    *reinterpret_cast<uint4*>(out.high_codes + cbase * cols + col0) = make_uint4(codes[0], codes[1], codes[2], codes[3]);
+  const int nsf_low = cols / (NV ? 16 : 32);
+  const int chunks_low = (nsf_low + 3) >> 2;
+  const int chunks_high = ((cols / 32) + 3) >> 2;
+  const int64_t rtiles = out.rows_pad >> 7;
+  const bool even = (part & 1) == 0;
+  if (NV || even) {
+    const int kb_low = NV ? part : (part >> 1);
+    if (out.scales_low) out.scales_low[rbase * nsf_low + kb_low] = static_cast<uint8_t>(sc_low);
+    if (out.sf_low_op) out.sf_low_op[sf_atom_offset(mat, orow, kb_low, rtiles, chunks_low)] = static_cast<uint8_t>(sc_low);
+  }
+  if (even) {
+    const int kb = part >> 1;
+    if (out.scales_high) out.scales_high[rbase * (cols / 32) + kb] = static_cast<uint8_t>(sc_high);
+    if (out.sf_high_op) out.sf_high_op[sf_atom_offset(mat, orow, kb, rtiles, chunks_high)] = static_cast<uint8_t>(sc_high);
+    if (GRAN == DMA_GRAN_BLOCK && out.quant_scale) out.quant_scale[rbase * (cols / 32) + kb] = sq;
+  }
+  if (part == 0) {
+    if (GRAN == DMA_GRAN_TOKEN && out.quant_scale) out.quant_scale[rbase] = sq;
+    if (GRAN == DMA_GRAN_TENSOR && out.quant_scale && row == 0) out.quant_scale[mat] = sq;
+    if (GRAN != DMA_GRAN_BLOCK && out.qs_f32) {
+      if (out.key_perm)
+        out.qs_f32[(mat * (out.rows_pad >> 7) + (row >> 7)) * kSqkTile +
+                   (out.key_perm == 1 ? perm_slot(static_cast<int>(row & 127)) : static_cast<int>(row & 127))] =
+            static_cast<float>(sq);
+      else
+        out.qs_f32[mat * out.rows_pad + row] = static_cast<float>(sq);
+    }
+  }
+}
+
+#ifndef DMA_QUANT_F64
+#define DMA_QUANT_F64 0  // 1: phase 1 runs q16_item (all float64) instead of q16_item_fast
+#endif
+
+template <typename T, bool NV, bool E5, int GRAN>
+__global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, int64_t n_mat, int64_t rows,
+                                                      int cols, int64_t mat_stride, int64_t row_stride,
+                                                      int is_query, double c,
+                                                      const unsigned long long* __restrict__ tensor_absmax,
+                                                      QuantOut out) {
+  // Work item = (matrix, block of 256 / tpr rows); a CTA walks items grid-stride
+  // (x over row blocks, y over matrices) and prefetches the next item's 32 input bytes
+  // while it quantizes the current one (the kernel is latency-bound otherwise).
+  const int lg_tpr = __ffs(cols >> 4) - 1;  // tpr = cols / 16, a power of two in [2, 32]
+  const int tpr = 1 << lg_tpr;
+  const int lane = threadIdx.x & 31;
+  const int part = threadIdx.x & (tpr - 1);
+  const int rpb = 256 >> lg_tpr;  // rows per block
+  const int64_t nbx = (rows + rpb - 1) / rpb;
+  const int rsub = threadIdx.x >> lg_tpr;
+  uint4 pf0 = make_uint4(0u, 0u, 0u, 0u), pf1 = pf0;  // prefetched words (bf16 inputs)
+  auto fetch = [&](int64_t m, int64_t b) {
+    const int64_t r = b * rpb + rsub;
+    if constexpr (sizeof(T) == 2) {
+      if (m < n_mat && r < rows) {
+        const uint4* src = reinterpret_cast<const uint4*>(x + m * mat_stride + r * row_stride + part * 16);
+        pf0 = __ldg(src);
+        pf1 = __ldg(src + 1);
+      } else {
+        pf0 = pf1 = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+  };
+  fetch(blockIdx.y, blockIdx.x);
+  for (int64_t mat = blockIdx.y; mat < n_mat; mat += gridDim.y) {
+  for (int64_t bx = blockIdx.x; bx < nbx; bx += gridDim.x) {
+  const int64_t row = bx * rpb + rsub;
+  const bool live = row < rows;  // whole rows live or die together (tpr | 32)
+  const uint4 cur0 = pf0, cur1 = pf1;
+  {
+    int64_t nb = bx + gridDim.x, nm = mat;
+    if (nb >= nbx) {
+      nb = blockIdx.x;
+      nm = mat + gridDim.y;
+    }
+    fetch(nm, nb);
+  }
+  if (__all_sync(0xffffffffu, !live)) continue;
+
+  if (DMA_QUANT_F64)
+    q16_item<T, NV, E5, GRAN>(x, mat_stride, row_stride, mat, rows, cols, row, live, part, tpr, lane, cur0, cur1,
+                              is_query, c, tensor_absmax, out);
+  else
+    q16_item_fast<T, NV, E5, GRAN>(x, mat_stride, row_stride, mat, rows, cols, row, live, part, tpr, lane, cur0,
+                                   cur1, is_query, c, tensor_absmax, out);
   }  // row-block loop
   }  // matrix loop
 }
@@ -684,14 +984,11 @@ __global__ void __launch_bounds__(256) quant_v2_kernel(const T* __restrict__ v, 
 // of one 32-key block (8-byte loads, 4-byte code stores; a warp covers 128 contiguous
 // columns of a key row).  Same arithmetic as quant_v2_kernel: the column maxima come
 // from the bf16 bit patterns (integer max), exact like the f32 max it replaces.
-static __global__ void __launch_bounds__(256) quant_v4_bf16_kernel(const __nv_bfloat16* __restrict__ v, int64_t keys, int dv,
-                                                            int64_t keys_pad, uint8_t* __restrict__ codes,
-                                                            uint8_t* __restrict__ sf_op) {
-  const int tpb = dv >> 2;                      // threads per key block
-  const int n = (threadIdx.x % tpb) * 4;        // first of my four columns
-  const int64_t kblk = static_cast<int64_t>(blockIdx.x) * (blockDim.x / tpb) + threadIdx.x / tpb;
-  const int64_t mat = blockIdx.y;
-  if (kblk * 32 >= keys_pad) return;
+// bf16 V -> MXFP8 along keys for one 32-key block (kblk) and four value columns n..n+3 of one
+// matrix (quant_v2_kernel arithmetic); shared by quant_v4_bf16_kernel and the fused kernel.
+__device__ __forceinline__ void qv4_block(const __nv_bfloat16* __restrict__ v, int64_t keys, int dv, int64_t keys_pad,
+                                          uint8_t* __restrict__ codes, uint8_t* __restrict__ sf_op, int64_t mat,
+                                          int64_t kblk, int n) {
   const __nv_bfloat16* src = v + mat * keys * dv + n;
   uint2 w[32];
 #pragma unroll
@@ -733,6 +1030,17 @@ static __global__ void __launch_bounds__(256) quant_v4_bf16_kernel(const __nv_bf
                         ((c & 127) >> 5) * 4 + (kblk & 3);
     sf_op[off] = static_cast<uint8_t>(e[j] + 127);
   }
+}
+
+static __global__ void __launch_bounds__(256) quant_v4_bf16_kernel(const __nv_bfloat16* __restrict__ v, int64_t keys, int dv,
+                                                            int64_t keys_pad, uint8_t* __restrict__ codes,
+                                                            uint8_t* __restrict__ sf_op) {
+  const int tpb = dv >> 2;                      // threads per key block
+  const int n = (threadIdx.x % tpb) * 4;        // first of my four columns
+  const int64_t kblk = static_cast<int64_t>(blockIdx.x) * (blockDim.x / tpb) + threadIdx.x / tpb;
+  const int64_t mat = blockIdx.y;
+  if (kblk * 32 >= keys_pad) return;
+  qv4_block(v, keys, dv, keys_pad, codes, sf_op, mat, kblk, n);
 }
 
 // Split-KV experiment (attn_sk.cuh, key_perm = 2): per 128-key tile of S_q^K (natural
