@@ -305,6 +305,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-n", type=int, default=32768, help="sequence length of the reference arm's sample heads")
     ap.add_argument("--fused", action="store_true", help="time the fused single-kernel forward")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay the forward from a captured CUDA graph (removes host launch cost: small configs)")
     ap.add_argument("--dry", action="store_true",
                     help="launcher / sharding / gather plumbing on CPU (gloo) with a stand-in compute; "
                          "prints the same JSON line shape (tests only, not a measurement)")
@@ -368,6 +370,22 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if args.graph:
+        # the same forward captured once (memset + kernels with their cached tensor maps) and
+        # replayed: device time without the per-call host work, for the small configurations
+        cs = torch.cuda.Stream()
+        cs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cs):
+            _lib.check(L.dma_attention_fwd(a, _lib.stream_ptr(cs)), "forward (capture)")
+        torch.cuda.synchronize()
+
+        def step():  # noqa: F811
+            graph.replay()
+
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
@@ -513,7 +531,7 @@ def main():
             "vs_baseline": None, "dtype": "mxfp8+nvfp4" if low == "nvfp4" else "mxfp8+mxfp4",
             "data": "synthetic (torch.randn bf16, seeded)",
             "config": cd,
-            "fused": fused,
+            "fused": fused, "graph": bool(args.graph),
             "phases_ms": {"forward": fwd_ms, "two_phase_quantize": quant_ms, "two_phase_attention": core_ms},
             "roofline": {"bound": "tensor", "kernel": ("dma_attn_pp_kernel<FUSE>" if fused else "dma_attn_pp_kernel")
                          if args.pv == "mxfp8" else "dma_attn_kernel", "achieved": achieved,

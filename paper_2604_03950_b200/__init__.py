@@ -20,4 +20,4 @@ from .attention import (  # noqa: F401
 from .softmax import OnlineSoftmaxState, apply_causal_mask, online_softmax_update  # noqa: F401
 from .metrics import MetricReport, high_precision_fraction, similarity  # noqa: F401
 from .decode import DmaKVCache  # noqa: F401
-from .scores import mixed_precision_scores, reference_attention, reference_scores  # noqa: F401
+from .scores import mixed_precision_scores, reference_attention, reference_scores, score_similarity  # noqa: F401

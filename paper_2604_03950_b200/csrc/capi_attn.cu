@@ -47,8 +47,54 @@ static CUtensorMapSwizzle swizzle_for(int row_bytes) {
 }
 
 // 3-D map over [mats][rows][inner] elements; box = [1][128][box_inner]
+// Encoded tensor maps are cached (small direct-mapped table keyed by every encode argument
+// and the device): repeated calls on the same buffers -- the serving / benchmark loop -- skip
+// the driver encode (5 per forward).
+struct MapKey {
+  const void* base;
+  int dev, dt, elem_bytes, box_inner;
+  int64_t inner, rows, mats;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && dev == o.dev && dt == o.dt && elem_bytes == o.elem_bytes && box_inner == o.box_inner &&
+           inner == o.inner && rows == o.rows && mats == o.mats;
+  }
+};
+struct MapSlot {
+  MapKey key;
+  CUtensorMap map;
+  bool valid;
+};
+static MapSlot g_map_cache[64];
+static std::mutex g_map_mutex;
+
+static int make_map_uncached(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem_bytes, int64_t inner,
+                             int64_t rows, int64_t mats, int box_inner);
+
 static int make_map(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem_bytes, int64_t inner,
                     int64_t rows, int64_t mats, int box_inner) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const MapKey key{base, dev, static_cast<int>(dt), elem_bytes, box_inner, inner, rows, mats};
+  const size_t h = (reinterpret_cast<uintptr_t>(base) >> 8) ^ (static_cast<size_t>(inner) * 31u) ^
+                   (static_cast<size_t>(rows) * 131u) ^ (static_cast<size_t>(mats) * 1031u) ^ static_cast<size_t>(box_inner);
+  MapSlot& slot = g_map_cache[h % 64];
+  {
+    std::lock_guard<std::mutex> lk(g_map_mutex);
+    if (slot.valid && slot.key == key) {
+      *m = slot.map;
+      return 0;
+    }
+  }
+  if (int rc = make_map_uncached(m, base, dt, elem_bytes, inner, rows, mats, box_inner)) return rc;
+  std::lock_guard<std::mutex> lk(g_map_mutex);
+  slot.key = key;
+  slot.map = *m;
+  slot.valid = true;
+  return 0;
+}
+
+static int make_map_uncached(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int elem_bytes, int64_t inner,
+                             int64_t rows, int64_t mats, int box_inner) {
   EncodeTiledFn fn = encode_fn();
   DMA_CHECK_ARG(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(mats)};

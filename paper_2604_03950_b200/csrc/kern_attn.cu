@@ -13,7 +13,7 @@ static int launch_attn(const AttnParams& p, int64_t items, cudaStream_t st) {
   using C = AttnCfg<D, DV, LOW, PVBF16>;
   auto kern = dma_attn_kernel<D, DV, LOW, PVBF16>;
   const int smem = C::kSmemBytes > 120 * 1024 ? C::kSmemBytes : 120 * 1024;  // one CTA per SM (TMEM 512 cols)
-  DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  DMA_SET_SMEM_ONCE(kern, smem);
   // persistent: one CTA per SM, items strided across CTAs (longest first)
   const int64_t grid = items < num_sms() ? items : num_sms();
   kern<<<static_cast<unsigned>(grid), 384, smem, st>>>(p);

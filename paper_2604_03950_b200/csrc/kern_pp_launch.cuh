@@ -16,7 +16,7 @@ static int launch_pp(const AttnParams& p, const PPParams& q, const FuseParams& f
   using C = PPCfg<D, DV, LOW>;
   auto kern = dma_attn_pp_kernel<D, DV, LOW, FUSE>;
   static_assert(C::kSmemBytes <= 227 * 1024, "smem budget");
-  DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+  DMA_SET_SMEM_ONCE(kern, C::kSmemBytes);
   const int grid = q.n_pairs < num_sms() ? q.n_pairs : num_sms();
   kern<<<static_cast<unsigned>(grid), C::kThreads, C::kSmemBytes, st>>>(p, q, fz);
   DMA_LAUNCH_CHECK();

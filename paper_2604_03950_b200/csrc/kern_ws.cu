@@ -12,7 +12,7 @@ template <int D, int DV, int LOW>
 static int launch_ws(const AttnParams& p, const SKParams& q, cudaStream_t st) {
   using C = WSCfg<D, DV, LOW>;
   auto kern = dma_attn_ws_kernel<D, DV, LOW>;
-  DMA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+  DMA_SET_SMEM_ONCE(kern, C::kSmemBytes);
   const int grid = q.n_items < num_sms() ? q.n_items : num_sms();
   kern<<<static_cast<unsigned>(grid), C::kThreads, C::kSmemBytes, st>>>(p, q);
   DMA_LAUNCH_CHECK();

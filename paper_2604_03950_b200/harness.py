@@ -211,16 +211,18 @@ def run_experiment(cfg: RunConfig) -> list[dict]:
 
     from .attention import dma_attention
     from .metrics import high_precision_fraction, similarity
-    from .scores import mixed_precision_scores, reference_attention, reference_scores
+    from .scores import mixed_precision_scores, reference_attention, reference_scores, score_similarity
 
     cfg.validate()
     q, k, v = load_inputs(cfg)
     heads, lq, d = q.shape
     lk = k.shape[1]
     qd, kd, vd = (torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (q, k, v))
+    # score targets above 2^24 cells per head use the row-blocked metric (no N x N matrices)
+    tiled = cfg.target == "scores" and lq * lk > (1 << 24)
     if cfg.target == "output":
         refs = [reference_attention(qd[h], kd[h], vd[h], causal=cfg.causal) for h in range(heads)]
-    else:
+    elif not tiled:
         refs = [reference_scores(qd[h], kd[h], causal=cfg.causal) for h in range(heads)]
     rows = []
     for fmt, diag, sink, gran in cfg.points():
@@ -228,11 +230,11 @@ def run_experiment(cfg: RunConfig) -> list[dict]:
         if cfg.target == "output":
             o = dma_attention(qd[None], kd[None], vd[None], acfg, out_dtype=torch.float32)[0]
             tests = [o[h] for h in range(heads)]
-        else:
+        elif not tiled:
             tests = [mixed_precision_scores(qd[h], kd[h], acfg) for h in range(heads)]
         hp = high_precision_fraction(lq, lk, cfg.tile_m, cfg.tile_n, diag, sink, cfg.causal)
         for h in range(heads):
-            m = similarity(refs[h], tests[h])
+            m = score_similarity(qd[h], kd[h], acfg) if tiled else similarity(refs[h], tests[h])
             rows.append({
                 "cos_sim": m.cos_sim, "rel_l1": m.rel_l1, "abs_l1": m.abs_l1, "rmse": m.rmse, "psnr": m.psnr,
                 "high_precision_pct": 100.0 * hp, "seed": None if cfg.q_path else cfg.seed,

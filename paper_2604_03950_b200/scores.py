@@ -117,5 +117,74 @@ def mixed_precision_scores(q, k, cfg: AttentionConfig):
     return _out(_softmax_rows(logits, base2=True), torch_in)
 
 
-__all__ = ["mixed_precision_scores", "reference_attention", "reference_scores"]
+def score_similarity(q, k, cfg: AttentionConfig, block_rows: int | None = None):
+    """``similarity(reference_scores(q, k, causal), mixed_precision_scores(q, k, cfg))``
+    (metrics.py:35-52 over attention.py:126-135 / 313-335) without the N x N matrices: the
+    two probability matrices are produced ``block_rows`` query rows at a time (softmax is
+    row-wise, and the row blocks are whole plan query tiles), and the metric sums
+    (dot, squared norms, L1 terms, squared error, peak) are accumulated per block in float64.
+    Memory is O(block_rows x Lk) instead of O(Lq x Lk): a 32K x 32K head needs ~0.3 GB, not
+    the 2 x 8.6 GB of the dense matrices.  Returns a ``MetricReport``."""
+    import torch
+
+    from .metrics import MetricReport
+
+    q, k = to_device_f64(q), to_device_f64(k)
+    _check_qkv(tuple(q.shape), tuple(k.shape), tuple(k.shape), cfg.causal)
+    if (cfg.low_format or cfg.high_format) and q.shape[1] % 32 != 0:
+        raise ValueError(f"head dim {q.shape[1]} not divisible by 32")
+    if not (torch.isfinite(q).all() and torch.isfinite(k).all()):
+        raise ValueError("quantize_dual: input contains non-finite values")
+    len_q, len_k, d = q.shape[0], k.shape[0], q.shape[1]
+    if block_rows is None:
+        block_rows = max(cfg.tile_m, (1 << 23) // max(len_k, 1) // cfg.tile_m * cfg.tile_m)
+    block_rows = max(cfg.tile_m, block_rows // cfg.tile_m * cfg.tile_m)
+    q_low, q_high, k_low, k_high = _operands(q, k, cfg)
+    plan_fn = causal_tile_plan if cfg.causal else noncausal_tile_plan
+    scale = 1.0 / math.sqrt(d)
+    kcols = torch.arange(len_k, device=q.device)
+    acc = torch.zeros(6, dtype=torch.float64, device=q.device)  # r.t, |r|^2, |t|^2, sum|r-t|, sum (r-t)^2, sum|r|
+    peak = torch.zeros((), dtype=torch.float64, device=q.device)
+    for r0 in range(0, len_q, block_rows):
+        r1 = min(r0 + block_rows, len_q)
+        qpos = torch.arange(r0, r1, device=q.device)[:, None]
+        # reference probabilities (base e, working precision) for rows r0:r1
+        lr = (q[r0:r1] @ k.T) * scale
+        if cfg.causal:
+            lr = torch.where(qpos >= kcols[None, :], lr, torch.full_like(lr, -math.inf))
+        ref = _softmax_rows(lr, base2=False)
+        del lr
+        # mixed-precision probabilities (base 2, per-tile precision) for the same rows
+        lt = torch.full((r1 - r0, len_k), -math.inf, dtype=torch.float64, device=q.device)
+        for q_tile in range(r0 // cfg.tile_m, -(-r1 // cfg.tile_m)):
+            q0, q1 = q_tile * cfg.tile_m, min((q_tile + 1) * cfg.tile_m, len_q)
+            for high in (False, True):
+                tiles = [t for t, h in plan_fn(q_tile, len_q, len_k, cfg) if h == high]
+                if not tiles:
+                    continue
+                cols = torch.cat([torch.arange(t * cfg.tile_n, min((t + 1) * cfg.tile_n, len_k), device=q.device)
+                                  for t in tiles])
+                block = (q_high if high else q_low)[q0:q1] @ (k_high if high else k_low)[cols].T
+                if cfg.causal:  # attention.py:178-184
+                    qp = torch.arange(q0, q1, device=q.device)[:, None]
+                    block = torch.where(qp >= cols[None, :], block, torch.full_like(block, -math.inf))
+                lt[q0 - r0:q1 - r0, cols] = block
+        tst = _softmax_rows(lt, base2=True)
+        del lt
+        diff = ref - tst
+        acc += torch.stack([(ref * tst).sum(), (ref * ref).sum(), (tst * tst).sum(), diff.abs().sum(),
+                            (diff * diff).sum(), ref.abs().sum()])
+        peak = torch.maximum(peak, ref.abs().max())
+        del ref, tst, diff
+    dot, rr, tt, abs_l1, sq, r_l1 = (float(x) for x in acc.tolist())
+    if rr == 0:
+        raise ValueError("metrics are undefined for an all-zero reference")
+    rn, tn = math.sqrt(rr), math.sqrt(tt)
+    rmse = math.sqrt(sq / (len_q * len_k))
+    pk = float(peak)
+    return MetricReport(cos_sim=dot / (rn * tn) if tn > 0 else 0.0, rel_l1=abs_l1 / r_l1, abs_l1=abs_l1, rmse=rmse,
+                        psnr=math.inf if rmse == 0 else 20.0 * math.log10(pk / rmse))
+
+
+__all__ = ["mixed_precision_scores", "reference_attention", "reference_scores", "score_similarity"]
 _ = np  # numpy inputs are accepted through to_device_f64

@@ -52,3 +52,33 @@ def test_reference_scores_and_attention(golden):
     t = D().reference_attention(torch.from_numpy(q), torch.from_numpy(k), torch.from_numpy(v), causal=False)
     assert t.is_cuda
     np.testing.assert_allclose(t.cpu().numpy(), golden["refattn_full"], rtol=1e-10, atol=1e-13)
+
+
+@pytest.mark.parametrize("case", [0, 1, 2])
+def test_score_similarity_tiled_matches_dense(case):
+    """score_similarity (row-blocked, no N x N buffers) == similarity of the dense matrices."""
+    name, lq, d, seed, kw = SCORE_CASES[case]
+    q, k = randn_bf16(seed, lq, d), randn_bf16(seed + 1, lq, d)
+    cfg = pkg_cfg(kw)
+    dense = D().similarity(D().reference_scores(q, k, causal=cfg.causal), D().mixed_precision_scores(q, k, cfg))
+    for rows in (cfg.tile_m, 3 * cfg.tile_m, None):
+        tiled = D().score_similarity(q, k, cfg, block_rows=rows)
+        for f in ("cos_sim", "rel_l1", "abs_l1", "rmse", "psnr"):
+            np.testing.assert_allclose(getattr(tiled, f), getattr(dense, f), rtol=1e-10, err_msg=f)
+
+
+def test_score_similarity_32k_without_dense_matrices():
+    """A c3-length head (N = 32768): the dense path would allocate 2 x 8.6 GB of float64
+    scores; the tiled metric stays under 1.5 GB of device memory."""
+    import torch
+
+    N, d = 32768, 128
+    q, k = randn_bf16(7, N, d), randn_bf16(8, N, d)
+    cfg = D().AttentionConfig(tile_m=128, tile_n=128, diag_window=128, sink_window=128)
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    base = torch.cuda.memory_allocated()
+    m = D().score_similarity(q, k, cfg)
+    peak = torch.cuda.max_memory_allocated() - base
+    assert peak < 1.5 * 2**30, peak
+    assert 0.9 < m.cos_sim <= 1.0 and 0 < m.rel_l1 < 1 and m.rmse > 0
