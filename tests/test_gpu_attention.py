@@ -4,8 +4,8 @@ Two references, two tolerances per PV mode:
 
 * the oracle exactly (``mixed_precision_attention`` of the reference, restated
   in oracle/; P and V stay float64 there, attention.py:174,250):
-    pv_mode="bf16"  (P, V in bf16; scores fp32)       rel-L2 <= 5e-3, max-abs <= 2e-2
-    pv_mode="mxfp8" (P -> E4M3 x2^8, V -> MXFP8/keys) rel-L2 <= 6e-2, max-abs <= 0.6
+    pv_mode="bf16"  (P, V in bf16; scores fp32)       rel-L2 <= 4.5e-3, max-abs <= 1e-2
+    pv_mode="mxfp8" (P -> E4M3 x2^4, V -> MXFP8/keys) rel-L2 <= 6e-2, max-abs <= 0.4
   (max-abs under MXFP8 PV is dominated by the first causal rows, where one or
   two quantized V rows carry the whole output: |v| ~ 4 x 2^-4 relative step);
 * the oracle with the kernel's stated PV quantization applied
@@ -26,7 +26,13 @@ from oracle import mx_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"bf16": (5e-3, 2e-2), "mxfp8": (6e-2, 0.6)}
+# vs the oracle = the reference algorithm, from the values measured over the parity suite
+# (profiles/r02_parity.jsonl): bf16 PV 2.05e-3 / 7.6e-3 (full-mantissa f64 inputs through the
+# INTEGRATION binding; 1.49e-3 / 3.14e-3 for bf16-representable inputs) -> 1.5x, max-abs at the
+# survey's 1e-2 cap; MXFP8 PV 3.99e-2 rel-L2 -> 6e-2, max-abs 0.359 (Dv = 128, first causal
+# row: one key, so the output IS the MXFP8 V row and its error is E4M3's 2^-4 relative step at
+# |v| ~ 5.7) -> 0.4, above the survey's 0.35, which the V quantization alone exceeds
+TOL = {"bf16": (4.5e-3, 1e-2), "mxfp8": (6e-2, 0.4)}
 TOL_EMU = {"bf16": (5e-4, 5e-3), "mxfp8": (5e-4, 5e-3)}
 
 
@@ -174,7 +180,7 @@ DEQ_CASES = [
     ("ident_high_256_d64", 256, 256, 64, "nvfp4", None, "tensor", 128, 0, True),
     ("ident_both_384", 384, 384, 128, None, None, "token", 0, 0, True),
 ]
-TOL_DEQ = {"bf16": (1e-2, 5e-2), "mxfp8": (6e-2, 0.6)}
+TOL_DEQ = {"bf16": (5e-3, 1e-2), "mxfp8": (6e-2, 0.4)}  # measured 2.92e-3 / 7.0e-3, 3.95e-2 / 0.227
 TOL_DEQ_EMU = {"bf16": (1e-2, 5e-2), "mxfp8": (3e-2, 0.15)}
 
 
@@ -269,6 +275,7 @@ def test_attention_value_dim_differs(d, dv, low, causal, pv):
     emu = O.mixed_precision_attention(q, k, v, oc, pv=pv)
     rel, mx = errs(got, want)
     erel, emx = errs(got, emu)
+    record_parity(f"dv_{d}_{dv}_{low}_{int(causal)}", pv, rel, mx, erel, emx)
     assert erel <= TOL_EMU[pv][0] and emx <= TOL_EMU[pv][1], (erel, emx)
     assert rel <= TOL[pv][0] and mx <= TOL[pv][1], (rel, mx)
 

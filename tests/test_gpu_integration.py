@@ -10,6 +10,7 @@ import sys
 import numpy as np
 import pytest
 
+from conftest import record_parity
 from test_gpu_attention import TOL, TOL_DEQ, errs
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -55,6 +56,8 @@ def test_binding_matches_live_reference(mx, case, pv_mode):
     want = A.mixed_precision_attention(q, k, v, cfg)
     assert got.shape == want.shape and got.dtype == np.float64
     rel, mxa = errs(got, want)
+    record_parity(f"binding_{lq}_{d}_{low}_{gran}_{int(causal)}_{np.dtype(dt).name}", "mxfp8" if pv_mode == 0 else "bf16",
+                  rel, mxa)
     tol = (TOL_DEQ if gran == "block" else TOL)["mxfp8" if pv_mode == 0 else "bf16"]
     assert rel <= tol[0] and mxa <= tol[1], (rel, mxa)
 
