@@ -105,6 +105,12 @@ constexpr bool kSplitPV = DMA_PP_SPLIT_PV != 0;
 // QK is issued as two N = 64 halves, the first overlapping the consumer's second-half load
 constexpr bool kHalfFree = DMA_PP_HALF_FREE != 0;
 
+#ifndef DMA_PP_EARLY_SF
+#define DMA_PP_EARLY_SF 0
+#endif
+// 1: the QK's scale-factor copies (and the K-tile wait) are issued before the S hand-over wait
+constexpr bool kEarlySF = DMA_PP_EARLY_SF != 0;
+
 #ifndef DMA_PP_EARLY_FREE
 #define DMA_PP_EARLY_FREE 0
 #endif
@@ -559,15 +565,21 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         bool hi;
         plan.entry(e, t, hi);
         if (LOW == kLowHigh) hi = true;
-        // the single S buffer: wait until its previous user copied it out
-        TRACE(true, 2, 26 + x);
-        PROF_MARK(0);
+        // the single S buffer: wait until its previous user copied it out.  With
+        // DMA_PP_EARLY_SF the scale-factor copies of this QK go first (off the S hand-over
+        // path): their TMEM slots were last read by this stream's previous QK, which had
+        // completed before the MMA warp passed the other stream's last s_free wait
         const uint32_t sfp = (su & 1) ^ 1;
-        ptx::mbar_wait(s_free, sfp);
-        PROF_MARK(3);
-        TRACE(true, 2, 10 + x);
-        ++su;
-        ptx::tc_fence_after();
+        auto wait_s_free = [&]() {
+          TRACE(true, 2, 26 + x);
+          PROF_MARK(0);
+          ptx::mbar_wait(s_free, sfp);
+          PROF_MARK(3);
+          TRACE(true, 2, 10 + x);
+          ++su;
+          ptx::tc_fence_after();
+        };
+        if (!kEarlySF) wait_s_free();
         const uint32_t oq = C::oQ + (qs * 2 + x) * C::kQStream;
         if (e == 0) {
           const uint32_t osfq = C::oSfQ + (qs * 2 + x) * C::kSfQ;
@@ -595,6 +607,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
           ptx::wu::tc_cp_sf(tmem + C::tSfK(x) + 4 * j, sf_desc(C::oSfK + kslt * 512 * C::kChK + 512 * j));
 #endif
         PROF_MARK(7);
+        if (kEarlySF) wait_s_free();
         TRACE(true, 2, 20 + x);
         const uint32_t tsfq = tmem + C::tSfQ(x), tsfk0 = tmem + C::tSfK(x);
         // one N = 128 QK, or two N = 64 halves (kHalfFree: the second waits for s_free[1]);

@@ -703,14 +703,6 @@ int dma_trace_read(unsigned long long* out, unsigned int* counts) {
   return 0;
 }
 #endif
-#ifdef DMA_PROFILE
-// profiling builds only: copy out and clear the softmax phase timers
-int dma_prof_read(unsigned long long* out, int n) {
-  DMA_CUDA_TRY(cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * (n < 32 ? n : 32)));
-  unsigned long long z[32] = {0};
-  DMA_CUDA_TRY(cudaMemcpyToSymbol(g_prof, z, sizeof(z)));
-  return 0;
-}
-#endif
+// (DMA_PROFILE builds: dma_prof_read lives in kern_pp.cu, next to the kernel's counters)
 
 }  // extern "C"

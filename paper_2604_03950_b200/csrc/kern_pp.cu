@@ -9,3 +9,14 @@ int run_pp(const AttnParams& p, const PPParams& q, int D, int DV, int low, cudaS
 }
 
 }  // namespace dma
+
+#ifdef DMA_PROFILE
+// profiling builds only: copy out and clear the ping-pong kernel's phase timers
+extern "C" int dma_prof_read(unsigned long long* out, int n) {
+  using namespace dma;
+  DMA_CUDA_TRY(cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * (n < 32 ? n : 32)));
+  static const unsigned long long z[32] = {0};
+  DMA_CUDA_TRY(cudaMemcpyToSymbol(g_prof, z, sizeof(z)));
+  return 0;
+}
+#endif
