@@ -629,17 +629,34 @@ __device__ __forceinline__ void q16_item_fast(const T* __restrict__ x, int64_t m
   }
   if (out.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(out.nonfinite, 1u);
 
-  // ---- scale decisions in float64, exactly as q16_item (quantize.py:98-106, 152-199)
-  double g;
-  if (GRAN == DMA_GRAN_TOKEN) {
-    g = shfl_max(amax, tpr);
-  } else if (GRAN == DMA_GRAN_BLOCK) {
-    g = shfl_max(amax, 2);
+  // ---- scale decisions in float64, exactly as q16_item (quantize.py:98-106, 152-199).
+  // The lane maxima are taken on the magnitudes' float32 bit patterns (exact and monotone
+  // for non-negative floats; one SHFL per step instead of a double's two) and the block
+  // maxima of x_scaled from the block maximum of |x| (x -> x c -> x / S_q are monotone
+  // roundings), so no double is shuffled for bf16 / f32 inputs.
+  double g, amax2;  // amax2: max |x| over the 32-column block (2 lanes)
+  if constexpr (sizeof(T) <= 4) {
+    const uint32_t mb = __float_as_uint(static_cast<float>(amax));
+    const uint32_t b2 = max(mb, __shfl_xor_sync(0xffffffffu, mb, 1));
+    uint32_t gb = b2;
+    if (GRAN == DMA_GRAN_TOKEN)
+      for (int o = 2; o < tpr; o <<= 1) gb = max(gb, __shfl_xor_sync(0xffffffffu, gb, o));
+    amax2 = static_cast<double>(__uint_as_float(b2));
+    g = GRAN == DMA_GRAN_TENSOR ? __longlong_as_double(static_cast<long long>(tensor_absmax[mat]))
+                                : static_cast<double>(__uint_as_float(gb));
   } else {
-    g = __longlong_as_double(static_cast<long long>(tensor_absmax[mat]));
+    amax2 = shfl_max(amax, 2);
+    if (GRAN == DMA_GRAN_TOKEN) {
+      g = shfl_max(amax2, tpr);
+    } else if (GRAN == DMA_GRAN_BLOCK) {
+      g = amax2;
+    } else {
+      g = __longlong_as_double(static_cast<long long>(tensor_absmax[mat]));
+    }
   }
   if (is_query) {
     amax = __dmul_rn(amax, c);
+    amax2 = __dmul_rn(amax2, c);
     g = __dmul_rn(g, c);
   }
   const double sq = g > 0.0 ? __ddiv_rn(g, 2688.0) : 1.0;
@@ -655,12 +672,12 @@ __device__ __forceinline__ void q16_item_fast(const T* __restrict__ x, int64_t m
     ysv = __drcp_rn(sv);
     sc_low = code;
   } else {
-    const double bm = shfl_max(amax, 2);  // 32-column block = 2 lanes, single level on x_sm
+    const double bm = amax2;  // 32-column block = 2 lanes, single level on x_sm
     const int e = bm > 0.0 ? min(max(floor_log2_pos(bm) - 2, -127), 127) : -127;
     inv = pow2(-e);
     sc_low = static_cast<uint32_t>(e + 127);
   }
-  const double hm = shfl_max(amax_sc, 2);
+  const double hm = qdiv<T>(amax2, sq, ysq);  // = the block max of |x_scaled|
   constexpr int kEmax = E5 ? 15 : 8;
   const int he = hm > 0.0 ? min(max(floor_log2_pos(hm) - kEmax, -127), 127) : -127;
   const double hinv = pow2(-he);
@@ -678,6 +695,7 @@ __device__ __forceinline__ void q16_item_fast(const T* __restrict__ x, int64_t m
     const float rsq = static_cast<float>(ysq);
     const float lf = static_cast<float>(lfac), hf = static_cast<float>(hinv);
     constexpr float kD = 0x1p-20f;
+    uint32_t d4acc[2] = {0u, 0u}, d8acc[4] = {0u, 0u, 0u, 0u};  // codes of the interval ends, XORed
 #pragma unroll
     for (int i = 0; i < 16; i += 2) {
       // x_sm (Q: x * c), x_scaled = x_sm / S_q.  The +0 addend of the first step turns an
@@ -690,19 +708,39 @@ __device__ __forceinline__ void q16_item_fast(const T* __restrict__ x, int64_t m
       const float2 l = NV ? __fmul2_rn(xsc, make_float2(lf, lf)) : __fmul2_rn(xsm, make_float2(lf, lf));
       const float2 lhi = __ffma2_rn(l, make_float2(kD, kD), l), llo = __ffma2_rn(l, make_float2(-kD, -kD), l);
       const uint32_t ma = ptx::cvt_e2m1x2(fabsf(lhi.x), fabsf(lhi.y)), mb = ptx::cvt_e2m1x2(fabsf(llo.x), fabsf(llo.y));
-      const uint32_t sg = ((__float_as_uint(l.x) >> 31) << 3) | ((__float_as_uint(l.y) >> 31) << 7);
-      packed[i >> 3] |= (ma | sg) << (4 * (i & 7));
+      // E2M1 sign bits 3 / 7 straight from the float32 sign bits (kept for rounded-to-zero values)
+      const uint32_t pb = ma | ((__float_as_uint(l.x) >> 28) & 0x08u) | ((__float_as_uint(l.y) >> 24) & 0x80u);
+      packed[i >> 3] |= pb << (4 * (i & 7));
       // 8-bit: x_scaled * 2^-he
       const float2 h = __fmul2_rn(xsc, make_float2(hf, hf));
       const float2 hhi = __ffma2_rn(h, make_float2(kD, kD), h), hlo = __ffma2_rn(h, make_float2(-kD, -kD), h);
       const uint32_t ha = E5 ? ptx::cvt_e5m2x2(fabsf(hhi.x), fabsf(hhi.y)) : ptx::cvt_e4m3x2(fabsf(hhi.x), fabsf(hhi.y));
       const uint32_t hb = E5 ? ptx::cvt_e5m2x2(fabsf(hlo.x), fabsf(hlo.y)) : ptx::cvt_e4m3x2(fabsf(hlo.x), fabsf(hlo.y));
-      // sign on nonzero magnitudes only (rounded-to-zero magnitudes stay +0)
-      const uint32_t hs = ((__float_as_uint(h.x) >> 31) << 7) | ((__float_as_uint(h.y) >> 31) << 15);
-      const uint32_t hcode = ha | (hs & __vcmpne4(ha, 0u));
-      codes[i >> 2] |= (hcode & 0xFFFFu) << (8 * (i & 3));
-      const uint32_t d4 = ma ^ mb, d8 = ha ^ hb;
-      fl |= ((((d4 & 0x0Fu) | (d8 & 0x00FFu)) != 0u ? 1u : 0u) | (((d4 & 0xF0u) | (d8 & 0xFF00u)) != 0u ? 2u : 0u)) << i;
+      // sign on nonzero magnitudes only (rounded-to-zero magnitudes stay +0): the two sign
+      // bytes by one PRMT, "magnitude byte >= 1" as bit 7 of byte + 0x7F (bytes <= 0x7E: no carry)
+      const uint32_t hs = __byte_perm(__float_as_uint(h.x), __float_as_uint(h.y), 0x0073u);
+      codes[i >> 2] |= (ha | (hs & (ha + 0x7F7Fu) & 0x8080u)) << (8 * (i & 3));
+      d4acc[i >> 3] |= (ma ^ mb) << (4 * (i & 7));
+      d8acc[i >> 2] |= (ha ^ hb) << (8 * (i & 3));
+    }
+    if ((d4acc[0] | d4acc[1] | d8acc[0] | d8acc[1] | d8acc[2] | d8acc[3]) != 0u) {
+      // element flags: nonzero nibbles of d4acc, nonzero bytes of d8acc, gathered to bits 0..15
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        uint32_t n = d4acc[w];
+        n |= n >> 1;
+        n |= n >> 2;
+        n &= 0x11111111u;
+        n = (n | (n >> 3)) & 0x03030303u;
+        n = (n | (n >> 6)) & 0x000F000Fu;
+        n = (n | (n >> 12)) & 0xFFu;
+        fl |= n << (8 * w);
+      }
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t b = __vcmpne4(d8acc[w], 0u) & 0x01010101u;
+        fl |= (((b * 0x01020408u) >> 24) & 0xFu) << (4 * w);
+      }
     }
   }
   {
