@@ -707,19 +707,18 @@ __device__ __forceinline__ void q16_item_fast(const T* __restrict__ x, int64_t m
       // 4-bit: NVFP4 x_scaled / sv, MXFP4 x_sm * 2^-e
       const float2 l = NV ? __fmul2_rn(xsc, make_float2(lf, lf)) : __fmul2_rn(xsm, make_float2(lf, lf));
       const float2 lhi = __ffma2_rn(l, make_float2(kD, kD), l), llo = __ffma2_rn(l, make_float2(-kD, -kD), l);
-      const uint32_t ma = ptx::cvt_e2m1x2(fabsf(lhi.x), fabsf(lhi.y)), mb = ptx::cvt_e2m1x2(fabsf(llo.x), fabsf(llo.y));
-      // E2M1 sign bits 3 / 7 straight from the float32 sign bits (kept for rounded-to-zero values)
-      const uint32_t pb = ma | ((__float_as_uint(l.x) >> 28) & 0x08u) | ((__float_as_uint(l.y) >> 24) & 0x80u);
-      packed[i >> 3] |= pb << (4 * (i & 7));
+      // signed conversions: RN is symmetric, and cvt keeps the sign of a negative value that
+      // rounds to zero (E2M1 -0 = 0x8: the reference's sign rule for the 4-bit codes)
+      const uint32_t ma = ptx::cvt_e2m1x2(lhi.x, lhi.y), mb = ptx::cvt_e2m1x2(llo.x, llo.y);
+      packed[i >> 3] |= ma << (4 * (i & 7));
       // 8-bit: x_scaled * 2^-he
       const float2 h = __fmul2_rn(xsc, make_float2(hf, hf));
       const float2 hhi = __ffma2_rn(h, make_float2(kD, kD), h), hlo = __ffma2_rn(h, make_float2(-kD, -kD), h);
-      const uint32_t ha = E5 ? ptx::cvt_e5m2x2(fabsf(hhi.x), fabsf(hhi.y)) : ptx::cvt_e4m3x2(fabsf(hhi.x), fabsf(hhi.y));
-      const uint32_t hb = E5 ? ptx::cvt_e5m2x2(fabsf(hlo.x), fabsf(hlo.y)) : ptx::cvt_e4m3x2(fabsf(hlo.x), fabsf(hlo.y));
-      // sign on nonzero magnitudes only (rounded-to-zero magnitudes stay +0): the two sign
-      // bytes by one PRMT, "magnitude byte >= 1" as bit 7 of byte + 0x7F (bytes <= 0x7E: no carry)
-      const uint32_t hs = __byte_perm(__float_as_uint(h.x), __float_as_uint(h.y), 0x0073u);
-      codes[i >> 2] |= (ha | (hs & (ha + 0x7F7Fu) & 0x8080u)) << (8 * (i & 3));
+      const uint32_t ha = E5 ? ptx::cvt_e5m2x2(hhi.x, hhi.y) : ptx::cvt_e4m3x2(hhi.x, hhi.y);
+      const uint32_t hb = E5 ? ptx::cvt_e5m2x2(hlo.x, hlo.y) : ptx::cvt_e4m3x2(hlo.x, hlo.y);
+      // rounded-to-zero magnitudes stay +0 (-0 = 0x80 -> 0x00): keep bit 7 of a byte only when
+      // its magnitude is >= 1 (bit 7 of magnitude + 0x7F; magnitudes <= 0x7E: no carry)
+      codes[i >> 2] |= (ha & (((ha & 0x7F7Fu) + 0x7F7Fu) | 0x7F7Fu)) << (8 * (i & 3));
       d4acc[i >> 3] |= (ma ^ mb) << (4 * (i & 7));
       d8acc[i >> 2] |= (ha ^ hb) << (8 * (i & 3));
     }
