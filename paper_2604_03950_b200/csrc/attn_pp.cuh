@@ -294,6 +294,21 @@ __device__ __forceinline__ float exp2_ordered(float x) {
 #endif
   return y;
 }
+#ifndef DMA_PP_EXP_INTERLEAVE
+#define DMA_PP_EXP_INTERLEAVE 0
+#endif
+// 1: the exp arguments' FFMA2 is issued inside the software-pipelined MUFU loop
+constexpr bool kExpInterleave = DMA_PP_EXP_INTERLEAVE != 0;
+__device__ __forceinline__ float2 ffma2_ordered(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm volatile(
+      "{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
 __device__ __forceinline__ uint32_t cvt_e4m3x2_ordered(float lo, float hi) {
 #ifdef DMA_EXP_NOCVT
   uint32_t r;
@@ -1031,11 +1046,13 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         // group q are interleaved with the F2FP packs of group q - 1
         const float2 rf2 = make_float2(rowf, rowf), b2 = make_float2(bias, bias);
         float2 ls = make_float2(0.f, 0.f);
+        if (!kExpInterleave) {
 #pragma unroll
-        for (int k2 = 0; k2 < NK; k2 += 2) {
-          const float2 v = __ffma2_rn(make_float2(tv[k2], tv[k2 + 1]), rf2, b2);
-          tv[k2] = v.x;
-          tv[k2 + 1] = v.y;
+          for (int k2 = 0; k2 < NK; k2 += 2) {
+            const float2 v = __ffma2_rn(make_float2(tv[k2], tv[k2 + 1]), rf2, b2);
+            tv[k2] = v.x;
+            tv[k2 + 1] = v.y;
+          }
         }
         uint32_t pk[8];
 #pragma unroll
@@ -1048,6 +1065,12 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
                 const float2 e2 = exp2_poly2(make_float2(tv[kk], tv[kk + 1]));
                 tv[kk] = e2.x;
                 tv[kk + 1] = e2.y;
+              } else if (kExpInterleave) {
+                // the argument FFMA2 issued in program order right before its MUFU pair (no
+                // 64-instruction prologue ahead of the first exp)
+                const float2 v = ffma2_ordered(make_float2(tv[kk], tv[kk + 1]), rf2, b2);
+                tv[kk] = exp2_ordered(v.x);
+                tv[kk + 1] = exp2_ordered(v.y);
               } else {
                 tv[kk] = exp2_ordered(tv[kk]);
                 tv[kk + 1] = exp2_ordered(tv[kk + 1]);

@@ -693,16 +693,7 @@ int dma_attention_set_fused(int on) {
   return prev;
 }
 
-#ifdef DMA_TRACE
-// tracing builds only: copy out and clear the CTA-0 event trace ([6][4096] + counts)
-int dma_trace_read(unsigned long long* out, unsigned int* counts) {
-  DMA_CUDA_TRY(cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 6 * 4096));
-  DMA_CUDA_TRY(cudaMemcpyFromSymbol(counts, g_trace_n, sizeof(unsigned int) * 6));
-  static const unsigned int z[6] = {0, 0, 0, 0, 0, 0};
-  DMA_CUDA_TRY(cudaMemcpyToSymbol(g_trace_n, z, sizeof(z)));
-  return 0;
-}
-#endif
+// (DMA_TRACE builds: dma_trace_read lives in kern_pp.cu, next to the kernel's trace buffer)
 // (DMA_PROFILE builds: dma_prof_read lives in kern_pp.cu, next to the kernel's counters)
 
 }  // extern "C"

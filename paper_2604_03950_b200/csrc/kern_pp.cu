@@ -20,3 +20,15 @@ extern "C" int dma_prof_read(unsigned long long* out, int n) {
   return 0;
 }
 #endif
+
+#ifdef DMA_TRACE
+// tracing builds only: copy out and clear the CTA-0 event trace ([6][4096] + counts)
+extern "C" int dma_trace_read(unsigned long long* out, unsigned int* counts) {
+  using namespace dma;
+  DMA_CUDA_TRY(cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 6 * 4096));
+  DMA_CUDA_TRY(cudaMemcpyFromSymbol(counts, g_trace_n, sizeof(unsigned int) * 6));
+  static const unsigned int z[6] = {0, 0, 0, 0, 0, 0};
+  DMA_CUDA_TRY(cudaMemcpyToSymbol(g_trace_n, z, sizeof(z)));
+  return 0;
+}
+#endif

@@ -85,3 +85,55 @@ mid = len(merged) // 2
 print("timeline (cycles since start):")
 for t, r, a in merged[mid:mid + 40]:
     print(f"  {t:10d} {['A', 'B', 'MMA', 'MMA2'][r]:>4s} {names.get(a, a)}")
+
+# MUFU occupancy: union of the two streams' exp intervals ("exp start" -> "exp end") over the
+# middle of the trace, and what each stream was doing when neither was in an exp phase
+def intervals(x):
+    e = ev[x]
+    out, st = [], None
+    for t, a in e:
+        if a == 4:
+            st = t
+        elif a == 5 and st is not None:
+            out.append((st, t))
+            st = None
+    return out
+
+
+ia, ib = intervals(0), intervals(1)
+if len(ia) > 20 and len(ib) > 20:
+    lo = max(ia[5][0], ib[5][0])
+    hi = min(ia[-5][1], ib[-5][1])
+    span = hi - lo
+    allv = sorted([(s, e_) for s, e_ in ia + ib if s >= lo and e_ <= hi])
+    covered, cur_s, cur_e, gaps = 0, None, None, []
+    for s_, e_ in allv:
+        if cur_e is None or s_ > cur_e:
+            if cur_e is not None:
+                covered += cur_e - cur_s
+                gaps.append((cur_e, s_))
+            cur_s, cur_e = s_, e_
+        else:
+            cur_e = max(cur_e, e_)
+    covered += cur_e - cur_s
+    both = 0
+    for s1, e1 in ia:
+        for s2, e2 in ib:
+            ov = min(e1, e2) - max(s1, s2)
+            if ov > 0 and s1 >= lo and e1 <= hi:
+                both += ov
+    glen = [b - a for a, b in gaps]
+    print(f"exp phases: A median {np.median([e_ - s for s, e_ in ia]):.0f} cyc, B median {np.median([e_ - s for s, e_ in ib]):.0f} cyc")
+    print(f"window {span} cyc: some stream in exp {covered / span * 100:.1f} %, both {both / span * 100:.1f} %, "
+          f"gaps {len(glen)} (median {np.median(glen) if glen else 0:.0f} cyc, total {sum(glen) / span * 100:.1f} %)")
+    # what each stream was doing at gap midpoints: its last event before the midpoint
+    from collections import Counter
+    for x in (0, 1):
+        c = Counter()
+        ts = [t for t, a in ev[x]]
+        for a, b in gaps:
+            mid = (a + b) // 2
+            i = bisect.bisect_right(ts, mid) - 1
+            if i >= 0:
+                c[names.get(ev[x][i][1], ev[x][i][1])] += 1
+        print(f"  stream {'AB'[x]} during gaps (last event before): {dict(c.most_common(5))}")
