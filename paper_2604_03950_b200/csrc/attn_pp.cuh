@@ -105,6 +105,12 @@ constexpr bool kSplitPV = DMA_PP_SPLIT_PV != 0;
 // QK is issued as two N = 64 halves, the first overlapping the consumer's second-half load
 constexpr bool kHalfFree = DMA_PP_HALF_FREE != 0;
 
+#ifndef DMA_PP_PV_LATE
+#define DMA_PP_PV_LATE 0
+#endif
+// 1: MMA issue order QK_A(e+1) PV_B(e-1) PV_A(e) QK_B(e+1) instead of QK_A(e+1) PV_A(e) QK_B(e+1) PV_B(e)
+constexpr bool kPvLate = DMA_PP_PV_LATE != 0;
+
 #ifndef DMA_PP_EARLY_SF
 #define DMA_PP_EARLY_SF 0
 #endif
@@ -126,6 +132,16 @@ constexpr bool kTurns = DMA_PP_TURNS != 0;
 // softmax warpgroups per stream: 1 = a thread owns a whole S row (128 columns);
 // 2 = two warps share each row, one key half each (4 softmax warps per SM sub-partition)
 constexpr int kSplit = DMA_PP_SPLIT;
+
+#ifndef DMA_PP_PSMEM
+#define DMA_PP_PSMEM 0
+#endif
+// 1: P goes through shared memory (E4M3, 128B-swizzled K-major, the PV MMA's A operand from
+// smem), double-buffered per stream, so a stream writes P(j) while PV(j-1) still reads P(j-1)
+// (no PV wait on the softmax chain).  Pays for the 64 KB with one Q slot per stream and a
+// 3-stage K ring.
+constexpr bool kPSmem = DMA_PP_PSMEM != 0 && kSplit == 1 && !kSplitPV;
+
 
 struct PPParams {
   int n_pairs;
@@ -220,7 +236,9 @@ __device__ __forceinline__ void fuse_acquire(const unsigned int* flag) {
 template <int D, int DV, int LOW>
 struct PPCfg {
   static constexpr int kBM = 128, kBN = 128;
-  static constexpr int kNK = kSplit == 2 ? 3 : 4, kNV = 3, kNS = 4, kNSch = 4;
+  static constexpr int kNK = (kSplit == 2 || kPSmem) ? 3 : 4, kNV = 3, kNS = 4, kNSch = 4;
+  static constexpr int kNQ = kPSmem ? 1 : 2;  // Q slots (pairs in flight)
+  static constexpr int kPBytes = 128 * 128;   // one P tile: 128 rows x 128 keys, E4M3
   static constexpr int kSoftWarps = 8 * kSplit;        // softmax warps (2 streams x kSplit warpgroups)
   static constexpr int kThreads = 32 * (kSoftWarps + 4);  // + producer, MMA issuer, 2 idle
   // setmaxnreg budgets: softmax warpgroups grow, the producer/MMA warpgroup shrinks.  The
@@ -239,11 +257,12 @@ struct PPCfg {
   static constexpr int kChK = kChHi > kChLo ? kChHi : kChLo;
   static constexpr int kSfQ = 512 * (kChHi + kChLo);
   // smem (offsets from a 1024-aligned base)
-  static constexpr int oQ = 0;                                // [2 slot][2 stream][kQStream]
-  static constexpr int oK = oQ + 4 * kQStream;                // [kNK][kKBytes]
+  static constexpr int oQ = 0;                                // [kNQ slot][2 stream][kQStream]
+  static constexpr int oK = oQ + 2 * kNQ * kQStream;          // [kNK][kKBytes]
   static constexpr int oV = oK + kNK * kKBytes;               // [kNV][kVBytes]
-  static constexpr int oSfQ = oV + kNV * kVBytes;             // [2 slot][2 stream][kSfQ]
-  static constexpr int oSfK = oSfQ + 4 * kSfQ;                // [kNK][kChK][512]
+  static constexpr int oP = oV + kNV * kVBytes;               // kPSmem: [2 stream][2 buf][kPBytes]
+  static constexpr int oSfQ = oP + (kPSmem ? 4 * kPBytes : 0);  // [kNQ slot][2 stream][kSfQ]
+  static constexpr int oSfK = oSfQ + 2 * kNQ * kSfQ;          // [kNK][kChK][512]
   static constexpr int oSfV = oSfK + kNK * kChK * 512;        // [kNV][512]
   static constexpr int kSqkBytes = 4 * kSqkTile;              // 576: S_q^K of one tile, bank-padded
   static constexpr int oSqK = oSfV + kNV * 512;               // [2 stream][kNS][kSqkBytes]
@@ -364,9 +383,9 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
   uint64_t* sq_empty = v_empty + C::kNV;          // [2][kNS]
   uint64_t* s_free = sq_empty + 2 * C::kNS;       // [2] S columns [0,64) / [64,128) copied out
   uint64_t* s_full = s_free + 2;                  // [2]
-  uint64_t* p_full = s_full + 2;                  // [2]
-  uint64_t* o_done = p_full + 2;                  // [2]
-  uint64_t* sch_full = o_done + 2;                // [kNSch]
+  uint64_t* p_full = s_full + 2;                  // [2 stream][2 buf] (kPSmem: per P buffer)
+  uint64_t* o_done = p_full + 4;                  // [2 stream][2 buf]
+  uint64_t* sch_full = o_done + 4;                // [kNSch]
   uint64_t* sch_empty = sch_full + C::kNSch;      // [kNSch]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sch_empty + C::kNSch);
   int* sched = reinterpret_cast<int*>(smem + C::oSch);
@@ -383,6 +402,8 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         ptx::mbar_init(s_full + i, 1);
         ptx::mbar_init(p_full + i, 4 * kSplit);
         ptx::mbar_init(o_done + i, 1);
+        ptx::mbar_init(p_full + 2 + i, 4 * kSplit);
+        ptx::mbar_init(o_done + 2 + i, 1);
       }
       for (int i = 0; i < C::kNK; ++i) {
         ptx::mbar_init(k_full + i, 1);
@@ -459,9 +480,9 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       const int mk[2] = {mat_k_of(p, bh[0]), ns == 2 ? mat_k_of(p, bh[1]) : -1};
       const bool shared_kv = ns == 2 && mk[0] == mk[1];
       // ---- Q (both streams) into the pair's slot
-      const int qs = po & 1;
+      const int qs = static_cast<int>(po % C::kNQ);
       PROF_MARK(0);
-      ptx::mbar_wait(q_empty + qs, ((po >> 1) & 1) ^ 1);
+      ptx::mbar_wait(q_empty + qs, ((po / C::kNQ) & 1) ^ 1);
       PROF_MARK(2);
       ++po;
       uint32_t qbytes = C::kQHiBytes + 512 * C::kChHi;
@@ -567,9 +588,9 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       if (plan.n == 0) continue;
       const int ns = bh[1] >= 0 ? 2 : 1;
       const bool shared_kv = ns == 2 && mat_k_of(p, bh[0]) == mat_k_of(p, bh[1]);
-      const int qs = po & 1;
+      const int qs = static_cast<int>(po % C::kNQ);
       PROF_MARK(0);
-      ptx::mbar_wait(q_full + qs, (po >> 1) & 1);
+      ptx::mbar_wait(q_full + qs, (po / C::kNQ) & 1);
       PROF_MARK(2);
       ++po;
       ptx::tc_fence_after();
@@ -676,7 +697,12 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
 
       auto issue_pv = [&](int x, int e) {
         PROF_MARK(0);
-        ptx::mbar_wait(p_full + x, pvc[x] & 1);
+        // kPSmem: P buffer pb of stream x (its PV count parity), barrier slot per buffer
+        const uint32_t pb = kPSmem ? (pvc[x] & 1) : 0u;
+        if (kPSmem)
+          ptx::mbar_wait(p_full + 2 * x + pb, (pvc[x] >> 1) & 1);
+        else
+          ptx::mbar_wait(p_full + x, pvc[x] & 1);
         PROF_MARK(5);
         TRACE(true, 2, 14 + x);
         ++pvc[x];
@@ -699,6 +725,18 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         const uint32_t vaddr = sbase + C::oV + vslt * C::kVBytes;
         constexpr int rb = DV;  // fp8 V row bytes (MN-major)
         const uint64_t dh = static_cast<uint64_t>(ptx::desc_hi(8 * rb, swz_mode(rb))) << 32;
+        if (kPSmem) {
+          // A = P from shared memory: 128 rows x 128 B, K-major, 128B swizzle (as the Q operand)
+          const uint32_t paddr = sbase + C::oP + (2 * x + pb) * C::kPBytes;
+          const uint64_t dhp = static_cast<uint64_t>(ptx::desc_hi(8 * 128, swz_mode(128))) << 32;
+#pragma unroll
+          for (int kk = 0; kk < C::kBN / 32; ++kk) {
+            const uint64_t ad = dhp | ptx::desc_lo(paddr + 32 * kk, 16);
+            const uint64_t bd = dh | ptx::desc_lo(vaddr + kk * 32 * rb, 16);
+            const uint32_t id = ptx::idesc_bs(0, 0, 0, 1, 128, DV, 1, kk & 3, kk & 3);
+            ptx::wu::mma_mxf8f6f4(tmem + C::tO(x), ad, bd, id, tmem + C::tSfP, tmem + C::tSfV(x), !(e == 0 && kk == 0));
+          }
+        } else {
 #pragma unroll
         for (int kk = 0; kk < C::kBN / 32; ++kk) {
           const uint64_t bd = dh | ptx::desc_lo(vaddr + kk * 32 * rb, 16);
@@ -706,10 +744,11 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
           ptx::wu::mma_mxf8f6f4_ts(tmem + C::tO(x), tmem + C::tP(x) + 8 * kk, bd, id, tmem + C::tSfP,
                                    tmem + C::tSfV(x), !(e == 0 && kk == 0));
         }
+        }
         PROF_MARK(8);
         TRACE(true, 2, 16 + x);
         if (x == ns - 1 || !shared_kv) ptx::wu::tc_commit(v_empty + vslt);
-        ptx::wu::tc_commit(o_done + x);
+        ptx::wu::tc_commit(o_done + (kPSmem ? 2 * x + pb : x));
         TRACE(true, 2, 24 + x);
         PROF_MARK(9);
       };
@@ -722,6 +761,18 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       } else {
       issue_qk(0, 0);
       if (ns == 2) issue_qk(1, 0);
+      if (kPvLate) {
+        // stream B's PV(e - 1) after QK_A(e + 1): the QK that gates the S hand-over is not
+        // queued behind four PV MMAs (measured slower with one P buffer per stream; with
+        // kPSmem the PV is off the softmax chain)
+        for (int e = 0; e < plan.n; ++e) {
+          if (e + 1 < plan.n) issue_qk(0, e + 1);
+          if (ns == 2 && e > 0) issue_pv(1, e - 1);
+          issue_pv(0, e);
+          if (ns == 2 && e + 1 < plan.n) issue_qk(1, e + 1);
+        }
+        if (ns == 2) issue_pv(1, plan.n - 1);
+      } else {
       for (int e = 0; e < plan.n; ++e) {
         if (e + 1 < plan.n) issue_qk(0, e + 1);
         issue_pv(0, e);
@@ -729,6 +780,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
           if (e + 1 < plan.n) issue_qk(1, e + 1);
           issue_pv(1, e);
         }
+      }
       }
       }
     }
@@ -1031,7 +1083,10 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         // P_x (and O_x) are read by PV(e-1): wait for it before overwriting.  Late wait:
         // just before the first P store, so the exps of key group 0 hide the wait
 #if !DMA_PP_LATE_PV_WAIT
-        if (e > 0) {
+        if (kPSmem) {
+          // P buffer g & 1 was read by PV(g - 2) (this stream's tile count g)
+          if (g >= 2) ptx::mbar_wait(o_done + 2 * x + (g & 1), ((g - 2) >> 1) & 1);
+        } else if (e > 0) {
           ptx::mbar_wait(o_done + x, (g - 1) & 1);
           ptx::tc_fence_after();
         }
@@ -1094,7 +1149,19 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
             ptx::tc_fence_after();
           }
 #endif
-          if (q4 > 0) ptx::tmem_st8(tmem + C::tP(x) + lane_base + NW * hh + 8 * (q4 - 1), pk);
+          if (q4 > 0) {
+            if (kPSmem) {
+              // row `row` of the 128B-swizzled K-major tile: 16-byte chunk c at c ^ (row & 7)
+              const uint32_t rbase = ptx::smem_u32(smem + C::oP + (2 * x + (g & 1)) * C::kPBytes) + row * 128;
+              const uint32_t c0 = 2 * (q4 - 1), c1 = c0 + 1;
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + ((c0 ^ (row & 7)) << 4)),
+                           "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]) : "memory");
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + ((c1 ^ (row & 7)) << 4)),
+                           "r"(pk[4]), "r"(pk[5]), "r"(pk[6]), "r"(pk[7]) : "memory");
+            } else {
+              ptx::tmem_st8(tmem + C::tP(x) + lane_base + NW * hh + 8 * (q4 - 1), pk);
+            }
+          }
         }
         if (kTurns && pair2) ptx::named_bar_arrive(2 - x, 256 * kSplit);
         TRACE(tw, x, 5);
@@ -1102,6 +1169,10 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         PROF_MARK(6);
         if (e > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
           // this thread's O columns *= alpha
+          if (kPSmem) {  // O holds PV(g - 1) once it completes
+            ptx::mbar_wait(o_done + 2 * x + ((g - 1) & 1), ((g - 1) >> 1) & 1);
+            ptx::tc_fence_after();
+          }
           const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
           for (int cq = 0; cq < OC / 32; ++cq) {
@@ -1120,8 +1191,9 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
+        if (kPSmem) ptx::fence_proxy_async_smem();  // P stores -> visible to the PV MMA (async proxy)
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(p_full + x);
+        if (lane == 0) ptx::mbar_arrive(kPSmem ? p_full + 2 * x + (g & 1) : p_full + x);
         TRACE(tw, x, 6);
         PROF_MARK(7);
       }
@@ -1136,7 +1208,10 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       }
       const float inv_l = 1.0f / (my_l > 0.f ? my_l : 1.0f);
       if (plan.n > 0) {
-        ptx::mbar_wait(o_done + x, (g - 1) & 1);
+        if (kPSmem)
+          ptx::mbar_wait(o_done + 2 * x + ((g - 1) & 1), ((g - 1) >> 1) & 1);
+        else
+          ptx::mbar_wait(o_done + x, (g - 1) & 1);
         ptx::tc_fence_after();
       }
       const uint32_t tO = tmem + C::tO(x) + lane_base + OC * hh;
