@@ -1112,4 +1112,76 @@ static __global__ void __launch_bounds__(256) sqk_tile_stats_kernel(float* __res
   }
 }
 
+// ------------------------------------------------------------------------
+// Phase 1 of the attention path in ONE launch (bf16 inputs, TOKEN granularity): CTAs
+// [0, nq) quantize Q, [nq, nq + nk) K -- each part a grid-stride walk over (matrix, row
+// block) items with the next item's 32 input bytes per thread prefetched, as
+// quant16_kernel -- and the remaining CTAs quantize V key blocks (qv4_block).  Saves two
+// launches per forward (small problems are launch-bound).
+// ------------------------------------------------------------------------
+struct P1Job {
+  const __nv_bfloat16* x;
+  int64_t n_mat, rows;
+  int is_query;
+  QuantOut out;
+};
+
+template <bool NV, bool E5>
+__device__ __forceinline__ void phase1_rows(const P1Job& j, int cols, double c, int cta, int ncta) {
+  const int lg_tpr = __ffs(cols >> 4) - 1;
+  const int tpr = 1 << lg_tpr;
+  const int lane = threadIdx.x & 31;
+  const int part = threadIdx.x & (tpr - 1);
+  const int rpb = 256 >> lg_tpr;
+  const int rsub = threadIdx.x >> lg_tpr;
+  const int64_t nbx = (j.rows + rpb - 1) / rpb;
+  const int64_t items = j.n_mat * nbx;
+  const int64_t mstride = j.rows * cols;
+  uint4 pf0 = make_uint4(0u, 0u, 0u, 0u), pf1 = pf0;
+  auto fetch = [&](int64_t it) {
+    const int64_t m = it / nbx, r = (it - m * nbx) * rpb + rsub;
+    if (it < items && r < j.rows) {
+      const uint4* src = reinterpret_cast<const uint4*>(j.x + m * mstride + r * cols + part * 16);
+      pf0 = __ldg(src);
+      pf1 = __ldg(src + 1);
+    } else {
+      pf0 = pf1 = make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+  fetch(cta);
+  for (int64_t it = cta; it < items; it += ncta) {
+    const uint4 cur0 = pf0, cur1 = pf1;
+    fetch(it + ncta);
+    const int64_t mat = it / nbx, row = (it - mat * nbx) * rpb + rsub;
+    const bool live = row < j.rows;
+    if (__all_sync(0xffffffffu, !live)) continue;
+    q16_item_fast<__nv_bfloat16, NV, E5, DMA_GRAN_TOKEN>(j.x, mstride, cols, mat, j.rows, cols, row, live, part, tpr,
+                                                        lane, cur0, cur1, j.is_query, c, nullptr, j.out);
+  }
+}
+
+template <bool NV, bool E5>
+__global__ void __launch_bounds__(256) phase1_bf16_kernel(const __grid_constant__ P1Job jq, const __grid_constant__ P1Job jk,
+                                                          int cols, double c, int nq, int nk,
+                                                          const __nv_bfloat16* __restrict__ v, int64_t keys, int dv,
+                                                          int64_t keys_pad, int64_t mk, uint8_t* __restrict__ v_codes,
+                                                          uint8_t* __restrict__ sf_v) {
+  const int b = blockIdx.x;
+  if (b < nq) {
+    phase1_rows<NV, E5>(jq, cols, c, b, nq);
+  } else if (b < nq + nk) {
+    phase1_rows<NV, E5>(jk, cols, c, b - nq, nk);
+  } else {
+    const int tpb = dv >> 2;                  // threads per 32-key block
+    const int kbpc = 256 / tpb;               // key blocks per CTA pass
+    const int64_t groups = (keys_pad / 32 + kbpc - 1) / kbpc;
+    const int nv = gridDim.x - nq - nk;
+    for (int64_t it = b - nq - nk; it < mk * groups; it += nv) {
+      const int64_t mat = it / groups;
+      const int64_t kblk = (it - mat * groups) * kbpc + threadIdx.x / tpb;
+      if (kblk * 32 < keys_pad) qv4_block(v, keys, dv, keys_pad, v_codes, sf_v, mat, kblk, (threadIdx.x % tpb) * 4);
+    }
+  }
+}
+
 }  // namespace dma
