@@ -111,6 +111,12 @@ constexpr bool kHalfFree = DMA_PP_HALF_FREE != 0;
 // 1: MMA issue order QK_A(e+1) PV_B(e-1) PV_A(e) QK_B(e+1) instead of QK_A(e+1) PV_A(e) QK_B(e+1) PV_B(e)
 constexpr bool kPvLate = DMA_PP_PV_LATE != 0;
 
+#ifndef DMA_FUSE_Q_PROLOGUE
+#define DMA_FUSE_Q_PROLOGUE 5
+#endif
+// eighths of the Q tiles quantized by all warps before the attention starts (fused kernel)
+constexpr int kFuseQPrologue = DMA_FUSE_Q_PROLOGUE;
+
 #ifndef DMA_PP_EARLY_SF
 #define DMA_PP_EARLY_SF 0
 #endif
@@ -183,7 +189,7 @@ __device__ __forceinline__ void fuse_publish(unsigned int* flag, int lane) {
 // row (q16_item_fast), 32 / tpr rows per pass, input bytes prefetched four passes ahead.  Out
 // of line: one copy of the quantizer code next to the attention code (instruction cache).
 template <int D, bool NV, bool E5>
-__device__ __noinline__ void fuse_quant_tile(const __nv_bfloat16* __restrict__ x, int64_t rows, int64_t mat, int t,
+__device__ __forceinline__ void fuse_quant_tile(const __nv_bfloat16* __restrict__ x, int64_t rows, int64_t mat, int t,
                                              int is_query, double c, const QuantOut& out, int lane) {
   constexpr int tpr = D / 16, rpp = 32 / tpr;
   const int part = lane & (tpr - 1), rsub = lane / tpr;
@@ -441,6 +447,69 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+
+  // Fused phase 1 (FUSE): one quantizer work queue -- K and V tiles (kv_role; kv-head major
+  // for head-major pair order, tile major otherwise) or Q tiles in the pair order.  One warp
+  // per 128-row tile (fuse_quant_tile / qv4_block), each tile published by its ready flag.
+  // items [first, last) of the queue, handed out by counters[ctr] (0: K/V, 1: the Q items the
+  // Q warps take, 2: the Q items of the prologue); a taken item is always processed
+  auto fuse_quant_loop = [&](bool kv_role, int ctr, int64_t first, int64_t last) {
+      const int mq = p.n_bh, mkn = p.n_bh / p.group;
+      const int64_t n_all = kv_role ? 2ll * mkn * rt_k : 2ll * pp.n_pairs;
+      const int64_t n_items = last < n_all ? last : n_all;
+      auto quant_tile = [&](const __nv_bfloat16* x, int64_t rows, int64_t mat, int t, int is_query, const QuantOut& out) {
+        if (fz.e5)
+          fuse_quant_tile<D, LOW != kLowMX4, true>(x, rows, mat, t, is_query, fz.c, out, lane);
+        else
+          fuse_quant_tile<D, LOW != kLowMX4, false>(x, rows, mat, t, is_query, fz.c, out, lane);
+      };
+      for (;;) {
+        unsigned int it = 0;
+        if (lane == 0) it = static_cast<unsigned int>(first) + atomicAdd(fz.counters + ctr, 1u);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (static_cast<int64_t>(it) >= n_items) break;
+        if (kv_role) {
+          const int kind = static_cast<int>(it & 1);  // 0 = K, 1 = V of the same tile
+          const int u = static_cast<int>(it >> 1);
+          int m, t;
+          if (pp.head_major) {
+            m = u / rt_k;
+            t = u - m * rt_k;
+          } else {
+            t = u / mkn;
+            m = u - t * mkn;
+          }
+          if (kind == 0) {
+            quant_tile(fz.k, p.lk, m, t, 0, fz.out_k);
+            fuse_publish(fz.flags + static_cast<int64_t>(mq) * rt_q + static_cast<int64_t>(m) * rt_k + t, lane);
+          } else {
+            // V: 4 key blocks of 32, DV / 4 lanes per block (qv4_block: 4 value columns per lane)
+            constexpr int tpb = DV / 4, bpp = 32 / tpb;
+            for (int kb = lane / tpb; kb < 4; kb += bpp)
+              qv4_block(fz.v, p.lk, DV, p.lk_pad, fz.v_codes, fz.sf_v, m, static_cast<int64_t>(t) * 4 + kb,
+                        (lane % tpb) * 4);
+            fuse_publish(fz.flags + static_cast<int64_t>(mq) * rt_q + static_cast<int64_t>(mkn + m) * rt_k + t, lane);
+          }
+        } else {
+          int bh[2], qt;
+          pair_coords(p, pp, static_cast<int>(it >> 1), bh[0], bh[1], qt);
+          const int b = bh[it & 1];
+          if (b < 0) continue;
+          quant_tile(fz.q, p.lq, b, qt, 1, fz.out_q);
+          fuse_publish(fz.flags + static_cast<int64_t>(b) * rt_q + qt, lane);
+        }
+      }
+  };
+  // prologue: every warp but the two quantizer warps drains the K / V queue first (the
+  // attention needs all K / V tiles of its first heads at once); warps 10 / 11 quantize Q in
+  // the pair order, overlapped with the attention
+  const int64_t fuse_q_pro = 2ll * pp.n_pairs * kFuseQPrologue / 8;  // Q items of the prologue
+  if (FUSE && warp != kMma + 1 && warp != kMma + 2) {
+    fuse_quant_loop(true, 0, 0, INT64_MAX);
+    // then the first kFuseQPrologue / 8 of the Q queue (the two Q warps alone cannot keep up
+    // with the attention on short pairs); the Q warps take the rest
+    fuse_quant_loop(false, 2, 0, fuse_q_pro);
+  }
 
   if (warp >= C::kSoftWarps) {
   // register budget: the last warpgroup gives registers to the softmax warpgroups (not when
@@ -787,56 +856,8 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
     PROF_MARK(0);
     PROF_FLUSH(10, 10);
   } else if (FUSE && (warp == kMma + 1 || warp == kMma + 2)) {
-    // =========================== fused phase 1: quantizer warps ===========================
-    // warp kMma + 1: K and V tiles, kv-head major (head-major pair order) or tile major;
-    // warp kMma + 2: Q tiles in the pair order.  One warp per 128-row tile: tpr = D / 16
-    // lanes per row (q16_item), 32 / tpr rows per pass, the next pass's 32 input bytes per
-    // lane prefetched while the current pass is quantized.
-    const int mq = p.n_bh, mkn = p.n_bh / p.group;
-    const bool kv_role = warp == kMma + 1;
-    const int64_t n_items = kv_role ? 2ll * mkn * rt_k : 2ll * pp.n_pairs;
-    auto quant_tile = [&](const __nv_bfloat16* x, int64_t rows, int64_t mat, int t, int is_query, const QuantOut& out) {
-      if (fz.e5)
-        fuse_quant_tile<D, LOW != kLowMX4, true>(x, rows, mat, t, is_query, fz.c, out, lane);
-      else
-        fuse_quant_tile<D, LOW != kLowMX4, false>(x, rows, mat, t, is_query, fz.c, out, lane);
-    };
-    for (;;) {
-      unsigned int it = 0;
-      if (lane == 0) it = atomicAdd(fz.counters + (kv_role ? 0 : 1), 1u);
-      it = __shfl_sync(0xffffffffu, it, 0);
-      if (static_cast<int64_t>(it) >= n_items) break;
-      if (kv_role) {
-        const int kind = static_cast<int>(it & 1);  // 0 = K, 1 = V of the same tile
-        const int u = static_cast<int>(it >> 1);
-        int m, t;
-        if (pp.head_major) {
-          m = u / rt_k;
-          t = u - m * rt_k;
-        } else {
-          t = u / mkn;
-          m = u - t * mkn;
-        }
-        if (kind == 0) {
-          quant_tile(fz.k, p.lk, m, t, 0, fz.out_k);
-          fuse_publish(fz.flags + static_cast<int64_t>(mq) * rt_q + static_cast<int64_t>(m) * rt_k + t, lane);
-        } else {
-          // V: 4 key blocks of 32, DV / 4 lanes per block (qv4_block: 4 value columns per lane)
-          constexpr int tpb = DV / 4, bpp = 32 / tpb;
-          for (int kb = lane / tpb; kb < 4; kb += bpp)
-            qv4_block(fz.v, p.lk, DV, p.lk_pad, fz.v_codes, fz.sf_v, m, static_cast<int64_t>(t) * 4 + kb,
-                      (lane % tpb) * 4);
-          fuse_publish(fz.flags + static_cast<int64_t>(mq) * rt_q + static_cast<int64_t>(mkn + m) * rt_k + t, lane);
-        }
-      } else {
-        int bh[2], qt;
-        pair_coords(p, pp, static_cast<int>(it >> 1), bh[0], bh[1], qt);
-        const int b = bh[it & 1];
-        if (b < 0) continue;
-        quant_tile(fz.q, p.lq, b, qt, 1, fz.out_q);
-        fuse_publish(fz.flags + static_cast<int64_t>(b) * rt_q + qt, lane);
-      }
-    }
+    // =========================== fused phase 1: Q quantizer warps ===========================
+    fuse_quant_loop(false, 1, fuse_q_pro, INT64_MAX);
   } else if (kSplitPV && (warp == kMma + 1 || warp == kMma + 2)) {
     // =========================== PV issuers (kSplitPV): warp kMma + 1 + x issues stream x's PVs ===========================
     // PV_x(e) depends only on P_x(e) and V, so it must not queue behind QK_x(e + 1), which
