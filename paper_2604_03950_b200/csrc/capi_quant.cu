@@ -20,12 +20,34 @@ const char* get_error() { return g_err; }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// DMA_QUANT32=0 selects the 16-column bf16 kernel (A/B and debugging)
+static bool quant32_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DMA_QUANT32");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <typename T, bool NV, bool E5, int GRAN>
 static void launch_rows(const DmaQuantArgs* a, const unsigned long long* tmax, const QuantOut& out,
                         cudaStream_t st) {
   const int64_t nrows = a->n_mat * a->rows;
   const int64_t tpr = a->cols / 16;
   if (tpr <= 32 && (tpr & (tpr - 1)) == 0 && a->row_stride % 8 == 0 && a->mat_stride % 8 == 0) {
+    if constexpr (sizeof(T) == 2) {
+      if (quant32_enabled()) {  // bf16: 32 columns per thread (q32_item_bf16)
+        const int64_t tpr32 = a->cols / 32;
+        const int64_t nbx = (a->rows * tpr32 + 255) / 256;
+        const int64_t by = a->n_mat < 65535 ? a->n_mat : 65535;
+        int64_t bx = (148 * 8 + by - 1) / by;
+        bx = bx < 1 ? 1 : (bx > nbx ? nbx : bx);
+        quant32_bf16_kernel<NV, E5, GRAN><<<dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), 256, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(a->x), a->n_mat, a->rows, static_cast<int>(a->cols), a->mat_stride,
+            a->row_stride, a->is_query, a->prescale, tmax, out);
+        return;
+      }
+    }
     // fast path: 16 columns per thread (cols in {32, 64, 128, 256, 512})
     // grid-stride over (row block, matrix) items: y covers the matrices (<= 65535),
     // x about 8 CTAs per SM in total so every CTA walks several row blocks (prefetching)

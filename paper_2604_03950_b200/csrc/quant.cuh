@@ -659,14 +659,14 @@ __device__ __forceinline__ void q16_item_fast(const T* __restrict__ x, int64_t m
     amax2 = __dmul_rn(amax2, c);
     g = __dmul_rn(g, c);
   }
-  const double sq = g > 0.0 ? __ddiv_rn(g, 2688.0) : 1.0;
+  const double sq = g > 0.0 ? qdiv<T>(g, 2688.0, 1.0 / 2688.0) : 1.0;
   const double ysq = __drcp_rn(sq);
   const double amax_sc = qdiv<T>(amax, sq, ysq);
   uint32_t sc_low;
   double sv = 1.0, ysv = 1.0, inv = 1.0;
   if (NV) {
     const double bm = amax_sc;
-    uint32_t code = bm > 0.0 ? e4m3_pos(__ddiv_rn(bm, 6.0)) : 0x38u;
+    uint32_t code = bm > 0.0 ? e4m3_pos(qdiv<T>(bm, 6.0, 1.0 / 6.0)) : 0x38u;
     if (code == 0 && bm > 0.0) code = 0x01;  // floor at 2^-9 (quantize.py:164-167)
     sv = decode_e4m3(code);
     ysv = __drcp_rn(sv);
@@ -819,9 +819,296 @@ __device__ __forceinline__ void q16_item_fast(const T* __restrict__ x, int64_t m
   }
 }
 
+// ------------------------------------------------------------------------
+// bf16 phase-1 variant with 32 columns per thread (one MX block = two NVFP4 blocks), so the
+// per-thread float64 scale decisions -- the instruction-bound part of q16_item_fast -- cover
+// twice the elements.  Same decisions and codes as q16_item_fast / q16_item:
+//   * float32 fast path with the +-2^-20 interval on every converted value; a pair of columns
+//     whose interval ends give different codes (an exact or near-exact rounding tie: x / S_q
+//     is a short number whenever S_q's mantissa shares factors with 2688 = 21 * 2^7, ~2.5 per
+//     128-column row) is flagged;
+//   * flagged pairs (or all 16 when the float32 guard fails) are recomputed in float64 one
+//     pair per lane per round and written over the fast codes with 1- / 2-byte stores after
+//     the row's vector stores (same thread, same address: program order);
+//   * sign rules: E2M1 keeps -0 for a negative value that rounds to zero, FP8 maps every zero
+//     magnitude to +0 (the word-wise fix after packing).
+// ------------------------------------------------------------------------
+constexpr double kRcp2688 = 1.0 / 2688.0;  // RN(1/2688): Markstein division by the constant
+constexpr double kRcp6 = 1.0 / 6.0;
+
+__device__ __forceinline__ uint32_t fp8_posz(uint32_t w) {  // bytes 0x80 -> 0x00
+  const uint32_t b = (w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;      // bit 7 set iff magnitude != 0
+  return w & (b | 0x7F7F7F7Fu);
+}
+
+template <bool NV, bool E5, int GRAN>
+__device__ __forceinline__ void q32_item_bf16(const __nv_bfloat16* __restrict__ x, int64_t mat_stride,
+                                              int64_t row_stride, int64_t mat, int64_t rows, int cols, int64_t row,
+                                              bool live, int part, int tpr, int lane, const uint32_t (&w)[16],
+                                              int is_query, double c,
+                                              const unsigned long long* __restrict__ tensor_absmax,
+                                              const QuantOut& out) {
+  // ---- maxima of |x| per 16-column half (the NVFP4 blocks) and per thread (the MX block)
+  uint32_t mm0 = w[0] & 0x7FFF7FFFu, mm1 = w[8] & 0x7FFF7FFFu;
+#pragma unroll
+  for (int i = 1; i < 8; ++i) {
+    mm0 = __vmaxu2(mm0, w[i] & 0x7FFF7FFFu);
+    mm1 = __vmaxu2(mm1, w[8 + i] & 0x7FFF7FFFu);
+  }
+  const uint32_t h0 = max(mm0 & 0xFFFFu, mm0 >> 16), h1 = max(mm1 & 0xFFFFu, mm1 >> 16);
+  const uint32_t hb = max(h0, h1);
+  if (out.nonfinite && __any_sync(0xffffffffu, hb >= 0x7F80u) && lane == 0) atomicOr(out.nonfinite, 1u);
+  double a0 = static_cast<double>(__uint_as_float(h0 << 16));
+  double a1 = static_cast<double>(__uint_as_float(h1 << 16));
+  double amax2 = static_cast<double>(__uint_as_float(hb << 16));
+  double g;
+  if (GRAN == DMA_GRAN_TOKEN) {
+    uint32_t gb = hb;
+    for (int o = 1; o < tpr; o <<= 1) gb = max(gb, __shfl_xor_sync(0xffffffffu, gb, o));
+    g = static_cast<double>(__uint_as_float(gb << 16));
+  } else if (GRAN == DMA_GRAN_BLOCK) {
+    g = amax2;
+  } else {
+    g = __longlong_as_double(static_cast<long long>(tensor_absmax[mat]));
+  }
+  if (is_query) {  // quantize.py:149; monotone rounding, so the max of x c is (max |x|) c
+    a0 = __dmul_rn(a0, c);
+    a1 = __dmul_rn(a1, c);
+    amax2 = __dmul_rn(amax2, c);
+    g = __dmul_rn(g, c);
+  }
+  // ---- scale decisions in float64 (quantize.py:98-106, 152-199)
+  const double sq = g > 0.0 ? mk_div(g, 2688.0, kRcp2688) : 1.0;
+  const double ysq = __drcp_rn(sq);
+  uint32_t sc_low;  // NV: the two E4M3 block scales (byte 0 = columns 0-15); MX: E8M0
+  double sv0 = 1.0, ysv0 = 1.0, sv1 = 1.0, ysv1 = 1.0, inv = 1.0;
+  if (NV) {
+    auto nv_scale = [&](double am, double& sv, double& ysv) -> uint32_t {
+      const double bm = mk_div(am, sq, ysq);  // block max of |x_scaled|
+      uint32_t code = bm > 0.0 ? e4m3_pos(mk_div(bm, 6.0, kRcp6)) : 0x38u;
+      if (code == 0 && bm > 0.0) code = 0x01;  // floor at 2^-9 (quantize.py:164-167)
+      sv = decode_e4m3(code);
+      ysv = __drcp_rn(sv);
+      return code;
+    };
+    sc_low = nv_scale(a0, sv0, ysv0);
+    sc_low |= nv_scale(a1, sv1, ysv1) << 8;
+  } else {
+    const int e = amax2 > 0.0 ? min(max(floor_log2_pos(amax2) - 2, -127), 127) : -127;
+    inv = pow2(-e);
+    sc_low = static_cast<uint32_t>(e + 127);
+  }
+  const double hm = mk_div(amax2, sq, ysq);  // block max of |x_scaled|
+  constexpr int kEmax = E5 ? 15 : 8;
+  const int he = hm > 0.0 ? min(max(floor_log2_pos(hm) - kEmax, -127), 127) : -127;
+  const double hinv = pow2(-he);
+  const uint32_t sc_high = static_cast<uint32_t>(he + 127);
+
+  // ---- float32 fast path
+  const double lfac0 = NV ? ysv0 : inv, lfac1 = NV ? ysv1 : inv;
+  const bool guard = sq >= 0x1p-100 && sq <= 0x1p+100 && (amax2 == 0.0 || (amax2 >= 0x1p-100 && amax2 <= 0x1p+100)) &&
+                     lfac0 >= 0x1p-120 && lfac0 <= 0x1p+120 && lfac1 >= 0x1p-120 && lfac1 <= 0x1p+120 &&
+                     hinv >= 0x1p-120 && hinv <= 0x1p+120;
+  uint32_t packed[4], codes[8];
+  uint32_t fl = 0xFFFFu;  // pairs to redo in float64
+  {
+    const float cf = is_query ? static_cast<float>(c) : 1.0f;
+    const float rsq = static_cast<float>(ysq);
+    const float lf0 = static_cast<float>(lfac0), lf1 = static_cast<float>(lfac1), hf = static_cast<float>(hinv);
+    constexpr float kD = 0x1p-20f;
+    uint32_t lb[16], hh[16], diff = 0u;
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      const float lf = p < 8 ? lf0 : lf1;
+      const float2 xv = make_float2(__uint_as_float(w[p] << 16), __uint_as_float(w[p] & 0xFFFF0000u));
+      // +0 addend: an input -0 becomes +0 (the reference's v < 0 tests see -0.0 as non-negative)
+      const float2 xsm = __ffma2_rn(xv, make_float2(cf, cf), make_float2(0.f, 0.f));
+      const float2 xsc = __fmul2_rn(xsm, make_float2(rsq, rsq));
+      const float2 l = NV ? __fmul2_rn(xsc, make_float2(lf, lf)) : __fmul2_rn(xsm, make_float2(lf, lf));
+      const float2 lhi = __ffma2_rn(l, make_float2(kD, kD), l), llo = __ffma2_rn(l, make_float2(-kD, -kD), l);
+      const uint32_t ma = ptx::cvt_e2m1x2(lhi.x, lhi.y), mb = ptx::cvt_e2m1x2(llo.x, llo.y);
+      const float2 h = __fmul2_rn(xsc, make_float2(hf, hf));
+      const float2 hhi = __ffma2_rn(h, make_float2(kD, kD), h), hlo = __ffma2_rn(h, make_float2(-kD, -kD), h);
+      const uint32_t ha = E5 ? ptx::cvt_e5m2x2(hhi.x, hhi.y) : ptx::cvt_e4m3x2(hhi.x, hhi.y);
+      const uint32_t hb2 = E5 ? ptx::cvt_e5m2x2(hlo.x, hlo.y) : ptx::cvt_e4m3x2(hlo.x, hlo.y);
+      lb[p] = ma;
+      hh[p] = ha;
+      diff |= ((ma ^ mb) | (ha ^ hb2)) != 0u ? (1u << p) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      packed[k] = lb[4 * k] | (lb[4 * k + 1] << 8) | (lb[4 * k + 2] << 16) | (lb[4 * k + 3] << 24);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) codes[k] = fp8_posz(hh[2 * k] | (hh[2 * k + 1] << 16));
+    if (guard) fl = diff;
+  }
+  if (!live) fl = 0u;
+
+  // ---- stores (as q16_item_fast)
+  const int64_t rbase = mat * rows + row;
+  const int64_t orow = out.key_perm == 1 ? ((row & ~int64_t(127)) | perm_row(static_cast<int>(row & 127))) : row;
+  const int64_t cbase = out.key_perm ? mat * out.rows_pad + orow : rbase;
+  const int col0 = part * 32;
+  if (live) {
+    if (out.packed_low)
+      *reinterpret_cast<uint4*>(out.packed_low + cbase * (cols / 2) + col0 / 2) =
+          make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    if (out.high_codes) {
+      uint4* hp = reinterpret_cast<uint4*>(out.high_codes + cbase * cols + col0);
+      hp[0] = make_uint4(codes[0], codes[1], codes[2], codes[3]);
+      hp[1] = make_uint4(codes[4], codes[5], codes[6], codes[7]);
+    }
+    const int nsf_low = cols / (NV ? 16 : 32);
+    const int chunks_low = (nsf_low + 3) >> 2;
+    const int chunks_high = ((cols / 32) + 3) >> 2;
+    const int64_t rtiles = out.rows_pad >> 7;
+    if (NV) {  // two adjacent scale bytes (block 2 part even: same 4-block chunk)
+      if (out.scales_low)
+        *reinterpret_cast<uint16_t*>(out.scales_low + rbase * nsf_low + 2 * part) = static_cast<uint16_t>(sc_low);
+      if (out.sf_low_op)
+        *reinterpret_cast<uint16_t*>(out.sf_low_op + sf_atom_offset(mat, orow, 2 * part, rtiles, chunks_low)) =
+            static_cast<uint16_t>(sc_low);
+    } else {
+      if (out.scales_low) out.scales_low[rbase * nsf_low + part] = static_cast<uint8_t>(sc_low);
+      if (out.sf_low_op) out.sf_low_op[sf_atom_offset(mat, orow, part, rtiles, chunks_low)] = static_cast<uint8_t>(sc_low);
+    }
+    if (out.scales_high) out.scales_high[rbase * (cols / 32) + part] = static_cast<uint8_t>(sc_high);
+    if (out.sf_high_op) out.sf_high_op[sf_atom_offset(mat, orow, part, rtiles, chunks_high)] = static_cast<uint8_t>(sc_high);
+    if (GRAN == DMA_GRAN_BLOCK && out.quant_scale) out.quant_scale[rbase * (cols / 32) + part] = sq;
+    if (part == 0) {
+      if (GRAN == DMA_GRAN_TOKEN && out.quant_scale) out.quant_scale[rbase] = sq;
+      if (GRAN == DMA_GRAN_TENSOR && out.quant_scale && row == 0) out.quant_scale[mat] = sq;
+      if (GRAN != DMA_GRAN_BLOCK && out.qs_f32) {
+        if (out.key_perm)
+          out.qs_f32[(mat * (out.rows_pad >> 7) + (row >> 7)) * kSqkTile +
+                     (out.key_perm == 1 ? perm_slot(static_cast<int>(row & 127)) : static_cast<int>(row & 127))] =
+              static_cast<float>(sq);
+        else
+          out.qs_f32[mat * out.rows_pad + row] = static_cast<float>(sq);
+      }
+    }
+  }
+
+  // ---- flagged pairs in float64 (q16_item's arithmetic), compacted over the warp: the
+  // flagged (lane, pair) items are listed in shared memory and every lane redoes one item per
+  // round with its owner's scales (shuffled), writing over the vector stores above (ordered
+  // after them by __syncwarp)
+  __shared__ uint16_t redo[8][32];  // (lane, pair) = lane * 16 + pair
+  uint16_t* slots = redo[threadIdx.x >> 5];
+  const uint32_t cnt = __popc(fl);
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0) return;
+  const int64_t xoff = mat * mat_stride + row * row_stride + col0;
+  for (uint32_t chunk = 0; chunk < total; chunk += 32) {
+    uint32_t f = fl, idx = incl - cnt;
+    while (f) {
+      const int p = __ffs(f) - 1;
+      f &= f - 1u;
+      if (idx >= chunk && idx < chunk + 32) slots[idx - chunk] = static_cast<uint16_t>(lane * 16 + p);
+      ++idx;
+    }
+    __syncwarp();
+    const bool work = lane < static_cast<int>(total - chunk);
+    const uint32_t item = work ? slots[lane] : static_cast<uint32_t>(lane * 16);
+    __syncwarp();
+    const int src = static_cast<int>(item >> 4), p = static_cast<int>(item & 15u);
+    const double psq = __shfl_sync(0xffffffffu, sq, src), pysq = __shfl_sync(0xffffffffu, ysq, src);
+    const double psv0 = __shfl_sync(0xffffffffu, sv0, src), pysv0 = __shfl_sync(0xffffffffu, ysv0, src);
+    const double psv1 = __shfl_sync(0xffffffffu, sv1, src), pysv1 = __shfl_sync(0xffffffffu, ysv1, src);
+    const double pinv = __shfl_sync(0xffffffffu, inv, src), phinv = __shfl_sync(0xffffffffu, hinv, src);
+    const int64_t pxoff = __shfl_sync(0xffffffffu, xoff, src), pcbase = __shfl_sync(0xffffffffu, cbase, src);
+    if (work) {
+      const int pcol0 = (src & (tpr - 1)) * 32;
+      const uint32_t wp = __ldg(reinterpret_cast<const uint32_t*>(x + pxoff) + p);
+      const double svp = p < 8 ? psv0 : psv1, ysvp = p < 8 ? pysv0 : pysv1;
+      uint32_t lc = 0u, hc = 0u;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double xv = __uint_as_float(e ? (wp & 0xFFFF0000u) : (wp << 16));
+        const double xs = is_query ? __dmul_rn(xv, c) : xv;  // quantize.py:149
+        const double xsc = mk_div(xs, psq, pysq);              // quantize.py:154
+        const double lv = NV ? mk_div(xsc, svp, ysvp) : xs * pinv;
+        const uint32_t l4 = (ptx::cvt_e2m1x2(rto_abs(lv), 0.f) & 0xFu) | (neg_nonzero(lv) ? 0x8u : 0u);
+        const double hv = xsc * phinv;
+        const float ha = rto_abs(hv);
+        uint32_t h8 = (E5 ? ptx::cvt_e5m2x2(ha, 0.f) : ptx::cvt_e4m3x2(ha, 0.f)) & 0xFFu;
+        if (h8 && neg_nonzero(hv)) h8 |= 0x80u;
+        lc |= l4 << (4 * e);
+        hc |= h8 << (8 * e);
+      }
+      if (out.packed_low) out.packed_low[pcbase * (cols / 2) + pcol0 / 2 + p] = static_cast<uint8_t>(lc);
+      if (out.high_codes)
+        *reinterpret_cast<uint16_t*>(out.high_codes + pcbase * cols + pcol0 + 2 * p) = static_cast<uint16_t>(hc);
+    }
+  }
+}
+
 #ifndef DMA_QUANT_F64
 #define DMA_QUANT_F64 0  // 1: phase 1 runs q16_item (all float64) instead of q16_item_fast
 #endif
+
+// bf16 phase 1 with q32_item_bf16: work item = (matrix, block of 256 / tpr rows), tpr =
+// cols / 32 threads per row; grid-stride like quant16_kernel, next item's 64 input bytes
+// prefetched.
+#ifndef DMA_Q32_MINB
+#define DMA_Q32_MINB 3  // min resident CTAs per SM for quant32_bf16_kernel (register cap)
+#endif
+template <bool NV, bool E5, int GRAN>
+__global__ void __launch_bounds__(256, DMA_Q32_MINB) quant32_bf16_kernel(const __nv_bfloat16* __restrict__ x, int64_t n_mat,
+                                                           int64_t rows, int cols, int64_t mat_stride,
+                                                           int64_t row_stride, int is_query, double c,
+                                                           const unsigned long long* __restrict__ tensor_absmax,
+                                                           QuantOut out) {
+  const int lg_tpr = __ffs(cols >> 5) - 1;
+  const int tpr = 1 << lg_tpr;
+  const int lane = threadIdx.x & 31;
+  const int part = threadIdx.x & (tpr - 1);
+  const int rpb = 256 >> lg_tpr;
+  const int64_t nbx = (rows + rpb - 1) / rpb;
+  const int rsub = threadIdx.x >> lg_tpr;
+  uint32_t pf[16];
+  auto fetch = [&](int64_t m, int64_t b) {
+    const int64_t r = b * rpb + rsub;
+    if (m < n_mat && r < rows) {
+      const uint4* src = reinterpret_cast<const uint4*>(x + m * mat_stride + r * row_stride + part * 32);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint4 v = __ldg(src + k);
+        pf[4 * k] = v.x; pf[4 * k + 1] = v.y; pf[4 * k + 2] = v.z; pf[4 * k + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) pf[k] = 0u;
+    }
+  };
+  fetch(blockIdx.y, blockIdx.x);
+  for (int64_t mat = blockIdx.y; mat < n_mat; mat += gridDim.y) {
+    for (int64_t bx = blockIdx.x; bx < nbx; bx += gridDim.x) {
+      const int64_t row = bx * rpb + rsub;
+      const bool live = row < rows;
+      uint32_t cur[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) cur[k] = pf[k];
+      {
+        int64_t nb = bx + gridDim.x, nm = mat;
+        if (nb >= nbx) {
+          nb = blockIdx.x;
+          nm = mat + gridDim.y;
+        }
+        fetch(nm, nb);
+      }
+      if (__all_sync(0xffffffffu, !live)) continue;
+      q32_item_bf16<NV, E5, GRAN>(x, mat_stride, row_stride, mat, rows, cols, row, live, part, tpr, lane, cur,
+                                  is_query, c, tensor_absmax, out);
+    }
+  }
+}
 
 template <typename T, bool NV, bool E5, int GRAN>
 __global__ void __launch_bounds__(256) quant16_kernel(const T* __restrict__ x, int64_t n_mat, int64_t rows,

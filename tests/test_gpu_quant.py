@@ -150,3 +150,58 @@ def test_quantize_dual_full_precision_inputs(dtype, gran):
         np.testing.assert_array_equal(t.packed_low.bytes_.cpu().numpy(), r.packed_low)
         np.testing.assert_array_equal(t.scales_low.cpu().numpy(), r.scales_low)
         np.testing.assert_array_equal(t.quant_scale.cpu().numpy().ravel(), np.asarray(r.quant_scale).ravel())
+
+
+def _np(a):
+    return a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+
+
+def _assert_same_t(t, r, key):
+    np.testing.assert_array_equal(_np(t.packed_low.bytes_), r.packed_low, err_msg=key + " packed_low")
+    np.testing.assert_array_equal(_np(t.scales_low), r.scales_low, err_msg=key + " scales_low")
+    np.testing.assert_array_equal(_np(t.high_codes), r.high_codes, err_msg=key + " high_codes")
+    np.testing.assert_array_equal(_np(t.scales_high), r.scales_high, err_msg=key + " scales_high")
+    np.testing.assert_array_equal(_np(t.quant_scale).view(np.uint64), np.asarray(r.quant_scale).view(np.uint64),
+                                  err_msg=key + " quant_scale")
+
+
+@pytest.mark.parametrize("lname", ["nvfp4", "mxfp4"])
+@pytest.mark.parametrize("hname", ["mxfp8_e4m3", "mxfp8_e5m2"])
+@pytest.mark.parametrize("gname", ["token", "block", "tensor"])
+@pytest.mark.parametrize("isq", [False, True])
+def test_quantize_dual_bf16_device_inputs(lname, hname, gname, isq):
+    """The forward's phase-1 kernel (bf16 device inputs: 32 columns per thread, float32 fast
+    path + float64 redo of flagged pairs) bit-exact against the oracle, on random rows, the
+    adversarial rows and rows whose maximum has a 21 * 2^k mantissa (many exact ties)."""
+    import torch
+
+    D = dma()
+    low, high = fmt_pair(lname, hname)
+    rng = np.random.default_rng(11)
+    ties = randn_bf16(12, 512, 128)
+    for i, m in enumerate((147, 168, 189, 210, 231, 252, 192, 224)):
+        ties[64 * i:64 * i + 64, 7] = m * 2.0 ** -6
+        ties[64 * i:64 * i + 64] = np.clip(ties[64 * i:64 * i + 64], -m * 2.0 ** -6, m * 2.0 ** -6)
+    ties[:, 20:40] = np.round(ties[:, 20:40] * 16) / 16  # short mantissas: exact quotients
+    x = np.concatenate([randn_bf16(7, 4096, 128), adversarial_rows(128), ties,
+                        randn_bf16(8, 33, 128, scale=float(rng.uniform(1e-3, 1e3)))])
+    xt = torch.from_numpy(x).to(torch.bfloat16)
+    x = xt.double().numpy()  # the oracle sees the bf16 values
+    t = D.quantize_dual(xt.cuda(), isq, low, high, getattr(D.Granularity, GR[gname]))
+    ol = {"nvfp4": O.NVFP4, "mxfp4": O.MXFP4}[lname]
+    oh = {"mxfp8_e4m3": O.MXFP8_E4M3, "mxfp8_e5m2": O.MXFP8_E5M2}[hname]
+    _assert_same_t(t, O.quantize_dual(x, isq, ol, oh, gname), f"bf16/{lname}/{hname}/{gname}/{isq}")
+
+
+@pytest.mark.parametrize("cols", [32, 64, 256, 512])
+def test_quantize_dual_bf16_widths(cols):
+    import torch
+
+    D = dma()
+    xt = torch.from_numpy(np.concatenate([randn_bf16(cols + 1, 301, cols, scale=2.0), adversarial_rows(cols)]))
+    xt = xt.to(torch.bfloat16)
+    x = xt.double().numpy()
+    for isq, gname in ((True, "token"), (False, "block")):
+        t = D.quantize_dual(xt.cuda(), isq, D.NVFP4, D.MXFP8_E4M3,
+                            getattr(D.Granularity, GR[gname]))
+        _assert_same_t(t, O.quantize_dual(x, isq, O.NVFP4, O.MXFP8_E4M3, gname), f"cols={cols}/{gname}")
