@@ -37,14 +37,21 @@ static void launch_rows(const DmaQuantArgs* a, const unsigned long long* tmax, c
   if (tpr <= 32 && (tpr & (tpr - 1)) == 0 && a->row_stride % 8 == 0 && a->mat_stride % 8 == 0) {
     if constexpr (sizeof(T) == 2) {
       if (quant32_enabled()) {  // bf16: 32 columns per thread (q32_item_bf16)
+        // contiguous matrices of whole 128-row tiles run as one matrix of n_mat * rows rows
+        // (every output offset is then the global row's; TENSOR needs the matrix index)
+        const bool flat = GRAN != DMA_GRAN_TENSOR && a->n_mat > 1 && a->mat_stride == a->rows * a->row_stride &&
+                          a->rows % 128 == 0 && out.rows_pad == a->rows;
+        const int64_t n_mat = flat ? 1 : a->n_mat, rows = flat ? a->n_mat * a->rows : a->rows;
         const int64_t tpr32 = a->cols / 32;
-        const int64_t nbx = (a->rows * tpr32 + 255) / 256;
-        const int64_t by = a->n_mat < 65535 ? a->n_mat : 65535;
+        const int64_t nbx = (rows * tpr32 + 255) / 256;
+        const int64_t by = n_mat < 65535 ? n_mat : 65535;
         int64_t bx = (148 * 8 + by - 1) / by;
         bx = bx < 1 ? 1 : (bx > nbx ? nbx : bx);
+        QuantOut o = out;
+        if (flat) o.rows_pad = rows;
         quant32_bf16_kernel<NV, E5, GRAN><<<dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), 256, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(a->x), a->n_mat, a->rows, static_cast<int>(a->cols), a->mat_stride,
-            a->row_stride, a->is_query, a->prescale, tmax, out);
+            static_cast<const __nv_bfloat16*>(a->x), n_mat, rows, static_cast<int>(a->cols), flat ? 0 : a->mat_stride,
+            a->row_stride, a->is_query, a->prescale, tmax, o);
         return;
       }
     }

@@ -847,7 +847,7 @@ __device__ __forceinline__ void q32_item_bf16(const __nv_bfloat16* __restrict__ 
                                               bool live, int part, int tpr, int lane, const uint32_t (&w)[16],
                                               int is_query, double c,
                                               const unsigned long long* __restrict__ tensor_absmax,
-                                              const QuantOut& out) {
+                                              const QuantOut& out, const double* rcp_tab) {
   // ---- maxima of |x| per 16-column half (the NVFP4 blocks) and per thread (the MX block)
   uint32_t mm0 = w[0] & 0x7FFF7FFFu, mm1 = w[8] & 0x7FFF7FFFu;
 #pragma unroll
@@ -885,10 +885,13 @@ __device__ __forceinline__ void q32_item_bf16(const __nv_bfloat16* __restrict__ 
   if (NV) {
     auto nv_scale = [&](double am, double& sv, double& ysv) -> uint32_t {
       const double bm = mk_div(am, sq, ysq);  // block max of |x_scaled|
-      uint32_t code = bm > 0.0 ? e4m3_pos(mk_div(bm, 6.0, kRcp6)) : 0x38u;
-      if (code == 0 && bm > 0.0) code = 0x01;  // floor at 2^-9 (quantize.py:164-167)
-      sv = decode_e4m3(code);
-      ysv = __drcp_rn(sv);
+      uint32_t code = e4m3_pos(mk_div(bm, 6.0, kRcp6));
+      code = bm > 0.0 ? max(code, 1u) : 0x38u;  // floor at 2^-9 (quantize.py:164-167)
+      // positive E4M3 value and its reciprocal: (1 + m/8) 2^(e-7) / m 2^-9, with
+      // 1/sv = RN(1/(1 + m/8)) 2^(7-e) / RN(1/m) 2^9 from the table (exact power-of-two scaling)
+      const int e = static_cast<int>(code >> 3), m = static_cast<int>(code & 7u);
+      sv = e ? __hiloint2double(((e + 1016) << 20) | (m << 17), 0) : m * 0x1p-9;
+      ysv = rcp_tab[e ? m : 8 + m] * pow2(e ? 7 - e : 9);
       return code;
     };
     sc_low = nv_scale(a0, sv0, ysv0);
@@ -989,12 +992,9 @@ __device__ __forceinline__ void q32_item_bf16(const __nv_bfloat16* __restrict__ 
     }
   }
 
-  // ---- flagged pairs in float64 (q16_item's arithmetic), compacted over the warp: the
-  // flagged (lane, pair) items are listed in shared memory and every lane redoes one item per
-  // round with its owner's scales (shuffled), writing over the vector stores above (ordered
-  // after them by __syncwarp)
-  __shared__ uint16_t redo[8][32];  // (lane, pair) = lane * 16 + pair
-  uint16_t* slots = redo[threadIdx.x >> 5];
+  // ---- flagged pairs in float64 (q16_item's arithmetic), compacted over the warp: every lane
+  // redoes one flagged (lane, pair) item per round with its owner's scales (shuffled), writing
+  // over the vector stores above (ordered after them by __syncwarp)
   const uint32_t cnt = __popc(fl);
   uint32_t incl = cnt;
 #pragma unroll
@@ -1004,20 +1004,33 @@ __device__ __forceinline__ void q32_item_bf16(const __nv_bfloat16* __restrict__ 
   }
   const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
   if (total == 0) return;
+  __syncwarp();  // the vector stores of every lane before any lane's corrections
   const int64_t xoff = mat * mat_stride + row * row_stride + col0;
+  const uint32_t base = incl - cnt;
   for (uint32_t chunk = 0; chunk < total; chunk += 32) {
-    uint32_t f = fl, idx = incl - cnt;
-    while (f) {
-      const int p = __ffs(f) - 1;
-      f &= f - 1u;
-      if (idx >= chunk && idx < chunk + 32) slots[idx - chunk] = static_cast<uint16_t>(lane * 16 + p);
-      ++idx;
+    // worker lane k takes item chunk + k: owner = the lane whose [base, incl) holds it (binary
+    // search on the inclusive counts), pair = the (item - base)-th set bit of the owner's mask
+    const uint32_t k = chunk + lane;
+    int lo = 0;
+#pragma unroll
+    for (int step = 16; step; step >>= 1) {
+      const uint32_t v = __shfl_sync(0xffffffffu, incl, lo + step - 1);
+      if (v <= k) lo += step;
     }
-    __syncwarp();
-    const bool work = lane < static_cast<int>(total - chunk);
-    const uint32_t item = work ? slots[lane] : static_cast<uint32_t>(lane * 16);
-    __syncwarp();
-    const int src = static_cast<int>(item >> 4), p = static_cast<int>(item & 15u);
+    const bool work = k < total;
+    const int src = work ? lo : lane;
+    uint32_t m = __shfl_sync(0xffffffffu, fl, src);
+    uint32_t r = k - __shfl_sync(0xffffffffu, base, src);  // rank of the pair in the owner's mask
+    int p = 0;
+#pragma unroll
+    for (int w = 8; w; w >>= 1) {  // select the r-th set bit of the 16-bit mask
+      const uint32_t c = __popc(m & ((1u << w) - 1u));
+      if (r >= c) {
+        r -= c;
+        m >>= w;
+        p += w;
+      }
+    }
     const double psq = __shfl_sync(0xffffffffu, sq, src), pysq = __shfl_sync(0xffffffffu, ysq, src);
     const double psv0 = __shfl_sync(0xffffffffu, sv0, src), pysv0 = __shfl_sync(0xffffffffu, ysv0, src);
     const double psv1 = __shfl_sync(0xffffffffu, sv1, src), pysv1 = __shfl_sync(0xffffffffu, ysv1, src);
@@ -1072,6 +1085,9 @@ __global__ void __launch_bounds__(256, DMA_Q32_MINB) quant32_bf16_kernel(const _
   const int rpb = 256 >> lg_tpr;
   const int64_t nbx = (rows + rpb - 1) / rpb;
   const int rsub = threadIdx.x >> lg_tpr;
+  __shared__ double rcp_tab[16];  // RN(1/(1 + m/8)) for m < 8, RN(1/(m - 8)) for m > 8
+  if (threadIdx.x < 16) rcp_tab[threadIdx.x] = threadIdx.x < 8 ? 8.0 / (8 + threadIdx.x) : 1.0 / (threadIdx.x - 8);
+  __syncthreads();
   uint32_t pf[16];
   auto fetch = [&](int64_t m, int64_t b) {
     const int64_t r = b * rpb + rsub;
@@ -1105,7 +1121,7 @@ __global__ void __launch_bounds__(256, DMA_Q32_MINB) quant32_bf16_kernel(const _
       }
       if (__all_sync(0xffffffffu, !live)) continue;
       q32_item_bf16<NV, E5, GRAN>(x, mat_stride, row_stride, mat, rows, cols, row, live, part, tpr, lane, cur,
-                                  is_query, c, tensor_absmax, out);
+                                  is_query, c, tensor_absmax, out, rcp_tab);
     }
   }
 }
