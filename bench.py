@@ -539,7 +539,7 @@ def main():
                          "traffic": traffic,
                          "peak_source": f"{src} bf16 {bf16:.0f} TF/s x (fp4 4x, fp8 2x) mix-weighted by Bit_high",
                          "peak_spec": peak_spec, "frac_of_spec": achieved / peak_spec},
-            "quant_phase": {"bound": "hbm", "kernels": "two-phase path: quant16_kernel x2 + quant_v4_bf16_kernel",
+            "quant_phase": {"bound": "hbm", "kernels": "two-phase path: quant32_bf16_kernel x2 (Q, K) + quant_v4_bf16_kernel (V)",
                             "algorithmic_bytes": qbytes, "achieved_gbs": qbytes / (quant_ms * 1e-3) / 1e9,
                             "peak_gbs": float(peaks["hbm_gbs"]),
                             "frac": qbytes / (quant_ms * 1e-3) / 1e9 / float(peaks["hbm_gbs"])},

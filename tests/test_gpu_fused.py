@@ -1,8 +1,9 @@
 """GPU: the fused forward (phase 1 inside the ping-pong kernel: quantizer warps + per-tile
 ready flags, attn_pp.cuh FuseParams) against the two-phase path (phase-1 kernels, then the
-attention kernel) on the same inputs.  Both quantize with the same device code (q16_item /
-qv4_block) into the same operand layouts and run the same attention code, so the outputs
-must be bit-identical; the fused call launches exactly one kernel."""
+attention kernel) on the same inputs.  Both quantize into the same operand layouts (the fused
+kernel with q16_item_fast / qv4_block, the two-phase path with the same code for small
+problems and quant32_bf16_kernel for large ones) and run the same attention code, so the
+outputs must be bit-identical; the fused call launches exactly one kernel."""
 
 import pytest
 
@@ -17,6 +18,11 @@ CASES = [
     (1, 2, 2, 512, 512, 128, 128, "MXFP8_E4M3", "MXFP8_E4M3", 0, 0, True),
     (1, 2, 1, 640, 640, 128, 64, "NVFP4", "MXFP8_E5M2", 128, 128, True),
     (1, 2, 2, 4096, 4096, 128, 128, "NVFP4", "MXFP8_E4M3", 128, 128, True),
+    # > 8 M phase-1 elements: the two-phase path runs quant32_bf16_kernel (32 columns per
+    # thread, warp-compacted float64 redo) -- flattened heads (N % 128 == 0) and per-head (ragged)
+    (1, 8, 2, 8192, 8192, 128, 128, "NVFP4", "MXFP8_E4M3", 128, 128, True),
+    (1, 6, 3, 7000, 7000, 128, 128, "MXFP4", "MXFP8_E5M2", 256, 128, True),
+    (2, 4, 4, 4096, 4608, 128, 128, "NVFP4", "MXFP8_E4M3", 128, 128, False),
 ]
 
 

@@ -1,6 +1,7 @@
 #!/bin/bash
 # Round-2 final evidence: full GPU suite (parity rows logged), smoke, bench lines for every config,
-# the c4 ablation sweep, launch list + full ncu capture of the attention and quantize kernels.
+# the c4 ablation sweep, launch list + full ncu capture of the attention and quantize kernels,
+# compute-sanitizer racecheck / synccheck / memcheck of the small cases.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 rm -f gpurun_out/parity_*.jsonl
@@ -16,6 +17,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:dma_attn_pp -s 3 -c 1 -o gpurun_out/r02_attn_full -f \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r02_ncu_attn.log 2>&1; tail -1 gpurun_out/r02_ncu_attn.log
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:quant16 -s 2 -c 1 -o gpurun_out/r02_quant_final -f \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:quant32 -s 2 -c 1 -o gpurun_out/r02_quant32_final -f \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r02_ncu_quant.log 2>&1; tail -1 gpurun_out/r02_ncu_quant.log
+for tool in racecheck synccheck memcheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_cases.py > gpurun_out/r02_sanitizer_$tool.log 2>&1
+  echo "$tool rc=$?"; tail -2 gpurun_out/r02_sanitizer_$tool.log
+done
 for f in gpurun_out/r02_bench_*.json; do echo "$f: $(head -c 300 $f)"; done
