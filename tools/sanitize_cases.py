@@ -17,6 +17,11 @@ k = torch.randn(1, 2, 384, 128, device="cuda").to(torch.bfloat16)
 v = torch.randn(1, 2, 384, 128, device="cuda").to(torch.bfloat16)
 base = dict(tile_m=128, tile_n=128, diag_window=128, sink_window=128)
 D.quantize_dual(q[0, 0], True, D.NVFP4, D.MXFP8_E4M3)
+x = torch.randn(512, 128, device="cuda")
+x[:, 3] = 168 / 32.0  # row maxima with a 21 * 2^k mantissa: many exact ties -> the warp-compacted redo
+x = x.clamp(-168 / 32.0, 168 / 32.0).to(torch.bfloat16)
+for low in (D.NVFP4, D.MXFP4):
+    D.quantize_dual(x, False, low, D.MXFP8_E4M3)
 print("quantize ok")
 D.dma_attention(q, k, v, D.AttentionConfig(**base))  # ping-pong kernel, two-phase
 print("pp ok")
