@@ -445,6 +445,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
   }
   ptx::tc_fence_before();
   __syncthreads();
+  ptx::pdl_wait();  // phase-1 outputs visible (PDL launch: the prologue above overlapped phase 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 

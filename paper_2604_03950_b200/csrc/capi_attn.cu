@@ -466,7 +466,12 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
     float* qs = reinterpret_cast<float*>(ws + (isq ? L.qs_q : L.qs_k));
     if (q.rows == 0) continue;
     const int kmode = (!isq && L.pp) ? ((use_sk_kernel() || use_ws_kernel()) ? 2 : 1) : 0;  // K operand layout
-    if (int rc = quantize_impl(&q, sfl, sfh, qs, isq ? L.lq_pad : L.lk_pad, st, kmode)) return rc;
+    // PDL: K's quantizer may start while Q's drains (independent outputs; the kernels chain
+    // their completion with pdl_wait, the attention kernel waits for the last)
+    g_pdl_next = !isq && pdl_enabled() && !L.tensor_gran;  // TENSOR: K reads its absmax kernel's result
+    const int qrc = quantize_impl(&q, sfl, sfh, qs, isq ? L.lq_pad : L.lk_pad, st, kmode);
+    g_pdl_next = false;
+    if (qrc) return qrc;
     g_launches += L.tensor_gran ? 2 : 1;
     if (kmode == 2 && use_sk_kernel()) {
       const int64_t nt = L.mk * (L.lk_pad / 128);
@@ -487,8 +492,9 @@ int attention_quantize(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaS
       if (a->in_dtype == DMA_DT_BF16) {
         const int kb4 = 256 / static_cast<int>(DV / 4);
         dim3 grid4(static_cast<unsigned>((L.lk_pad / 32 + kb4 - 1) / kb4), static_cast<unsigned>(L.mk));
-        quant_v4_bf16_kernel<<<grid4, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(a->v), a->len_k,
-                                                   static_cast<int>(DV), L.lk_pad, ws + L.v_codes, ws + L.sf_v);
+        DMA_CUDA_TRY(launch_kernel(pdl_enabled(), quant_v4_bf16_kernel, grid4, dim3(256), 0, s,
+                                   static_cast<const __nv_bfloat16*>(a->v), a->len_k, static_cast<int>(DV), L.lk_pad,
+                                   ws + L.v_codes, ws + L.sf_v));
       }
       else if (a->in_dtype == DMA_DT_F32)
         quant_v2_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(a->v), a->len_k, static_cast<int>(DV),

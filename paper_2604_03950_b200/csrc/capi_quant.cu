@@ -10,6 +10,15 @@
 namespace dma {
 
 static thread_local char g_err[1024] = "";
+thread_local bool g_pdl_next = false;
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DMA_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 void set_error(const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
@@ -49,9 +58,11 @@ static void launch_rows(const DmaQuantArgs* a, const unsigned long long* tmax, c
         bx = bx < 1 ? 1 : (bx > nbx ? nbx : bx);
         QuantOut o = out;
         if (flat) o.rows_pad = rows;
-        quant32_bf16_kernel<NV, E5, GRAN><<<dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)), 256, 0, st>>>(
-            static_cast<const __nv_bfloat16*>(a->x), n_mat, rows, static_cast<int>(a->cols), flat ? 0 : a->mat_stride,
-            a->row_stride, a->is_query, a->prescale, tmax, o);
+        const cudaError_t e = launch_kernel(
+            g_pdl_next, quant32_bf16_kernel<NV, E5, GRAN>, dim3(static_cast<unsigned>(bx), static_cast<unsigned>(by)),
+            dim3(256), 0, st, static_cast<const __nv_bfloat16*>(a->x), n_mat, rows, static_cast<int>(a->cols),
+            flat ? 0 : a->mat_stride, a->row_stride, a->is_query, a->prescale, tmax, o);
+        if (e != cudaSuccess) set_error("quant32 launch: %s", cudaGetErrorString(e));
         return;
       }
     }

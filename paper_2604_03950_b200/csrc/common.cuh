@@ -32,6 +32,27 @@ const char* get_error();
 
 #define DMA_LAUNCH_CHECK() DMA_CUDA_TRY(cudaGetLastError())
 
+// Kernel launch with the programmatic-stream-serialization attribute when `pdl` (the kernel
+// may start while the previous kernel in the stream drains; it must ptx::pdl_wait() before
+// touching that kernel's results).  pdl_enabled(): env DMA_PDL=0 turns it off (A/B, debug).
+bool pdl_enabled();
+extern thread_local bool g_pdl_next;  // set around quantize_impl: launch its kernel with PDL
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                 cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) {
   // ceil(a / b) for b > 0 and any sign of a
   return (a >= 0) ? (a + b - 1) / b : -((-a) / b);

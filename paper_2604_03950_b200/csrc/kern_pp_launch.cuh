@@ -18,8 +18,11 @@ static int launch_pp(const AttnParams& p, const PPParams& q, const FuseParams& f
   static_assert(C::kSmemBytes <= 227 * 1024, "smem budget");
   DMA_SET_SMEM_ONCE(kern, C::kSmemBytes);
   const int grid = q.n_pairs < num_sms() ? q.n_pairs : num_sms();
-  kern<<<static_cast<unsigned>(grid), C::kThreads, C::kSmemBytes, st>>>(p, q, fz);
-  DMA_LAUNCH_CHECK();
+  // PDL: the prologue (barriers, TMEM, descriptor prefetch) overlaps phase 1's tail; the
+  // kernel pdl_waits before its first read of phase-1 data (the fused kernel has no
+  // producer kernel before it: the attribute is then a no-op)
+  DMA_CUDA_TRY(launch_kernel(pdl_enabled() && !FUSE, kern, dim3(static_cast<unsigned>(grid)), dim3(C::kThreads),
+                             C::kSmemBytes, st, p, q, fz));
   return 0;
 }
 

@@ -1103,6 +1103,7 @@ __global__ void __launch_bounds__(256, DMA_Q32_MINB) quant32_bf16_kernel(const _
       for (int k = 0; k < 16; ++k) pf[k] = 0u;
     }
   };
+  ptx::pdl_launch_dependents();
   fetch(blockIdx.y, blockIdx.x);
   for (int64_t mat = blockIdx.y; mat < n_mat; mat += gridDim.y) {
     for (int64_t bx = blockIdx.x; bx < nbx; bx += gridDim.x) {
@@ -1124,6 +1125,9 @@ __global__ void __launch_bounds__(256, DMA_Q32_MINB) quant32_bf16_kernel(const _
                                   is_query, c, tensor_absmax, out, rcp_tab);
     }
   }
+  // PDL chain (forward's phase 1: Q, K, V kernels overlap; the attention kernel waits for the
+  // last one): this grid completes only after the previous kernel in the stream
+  ptx::pdl_wait();
 }
 
 template <typename T, bool NV, bool E5, int GRAN>
@@ -1379,8 +1383,9 @@ static __global__ void __launch_bounds__(256) quant_v4_bf16_kernel(const __nv_bf
   const int n = (threadIdx.x % tpb) * 4;        // first of my four columns
   const int64_t kblk = static_cast<int64_t>(blockIdx.x) * (blockDim.x / tpb) + threadIdx.x / tpb;
   const int64_t mat = blockIdx.y;
-  if (kblk * 32 >= keys_pad) return;
-  qv4_block(v, keys, dv, keys_pad, codes, sf_op, mat, kblk, n);
+  ptx::pdl_launch_dependents();
+  if (kblk * 32 < keys_pad) qv4_block(v, keys, dv, keys_pad, codes, sf_op, mat, kblk, n);
+  ptx::pdl_wait();  // PDL chain: this grid completes only after the previous phase-1 kernel
 }
 
 // Split-KV experiment (attn_sk.cuh, key_perm = 2): per 128-key tile of S_q^K (natural
@@ -1470,6 +1475,7 @@ __global__ void __launch_bounds__(256) phase1_bf16_kernel(const __grid_constant_
                                                           int64_t keys_pad, int64_t mk, uint8_t* __restrict__ v_codes,
                                                           uint8_t* __restrict__ sf_v) {
   const int b = blockIdx.x;
+  ptx::pdl_launch_dependents();
   if (b < nq) {
     phase1_rows<NV, E5>(jq, cols, c, b, nq);
   } else if (b < nq + nk) {
