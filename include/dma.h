@@ -128,7 +128,11 @@ typedef struct {
   int64_t batch, heads, kv_heads, len_q, len_k, head_dim, v_dim;
   int32_t tile_m, tile_n, diag_window, sink_window, causal;
   int32_t low_format, high_format, granularity, pv_mode;
-  int32_t _pad;
+  /* KV splits for this call (dma_attention_set_kv_split): 0 = the library's policy (default),
+   * 1 = unsplit, n >= 2 = n splits (capped by the plan length and 16).  A caller that cuts
+   * one problem into pieces passes the whole problem's count (dma_attention_kv_split) so the
+   * pieces reproduce its output bit for bit.  (Formerly padding: old callers pass 0.) */
+  int32_t kv_split;
   double prescale; /* log2(e)/sqrt(head_dim), float64 */
   void* workspace;
   size_t workspace_bytes;
@@ -212,6 +216,18 @@ int dma_last_launch_count(void);
  * kernel per call; bf16 inputs, TOKEN granularity, block-scaled PV): 1 on, 0 off (default,
  * the two-phase path is faster on B200).  Returns the previous setting. */
 int dma_attention_set_fused(int on);
+
+/* KV splits of the ping-pong forward for small problems (fewer head pairs x query tiles
+ * than SMs): each pair's tile plan (attention.py:191-233) is cut into ranges of >= 2 key
+ * tiles processed by different CTAs and merged in the kernel (same online-softmax algebra
+ * as attention.py:150-175 across the ranges).  mode: -1 auto (default), 0 or 1 off, n >= 2
+ * force n splits (capped by the plan length and 16).  Also DMA_KV_SPLIT.  Returns the
+ * previous mode. */
+int dma_attention_set_kv_split(int mode);
+
+/* The KV split count dma_attention_fwd uses for `a` under the current mode (1 = unsplit),
+ * -1 on invalid arguments. */
+int dma_attention_kv_split(const DmaAttnArgs* a);
 
 #ifdef __cplusplus
 }

@@ -466,7 +466,7 @@ def _quantize_p(p: np.ndarray, pv: str) -> np.ndarray:
     return p
 
 
-def mixed_precision_attention(q, k, v, cfg: Cfg, pv: str = "f64", q_tiles=None) -> np.ndarray:
+def mixed_precision_attention(q, k, v, cfg: Cfg, pv: str = "f64", q_tiles=None, kv_split: int = 1) -> np.ndarray:
     """Tile loop + base-2 online softmax (attention.py:150-175, 178-184, 282-310).
 
     ``pv="f64"`` is the reference exactly.  ``pv="mxfp8"`` / ``"bf16"`` add the
@@ -474,7 +474,12 @@ def mixed_precision_attention(q, k, v, cfg: Cfg, pv: str = "f64", q_tiles=None) 
     along keys and lazy max rescaling, or P and V in bf16) on top of the same
     algorithm; the row sum l still uses the unquantized P, as the kernel does.
     ``q_tiles`` (optional): compute only these query tiles (rows of other tiles are NaN),
-    for sampled checks at full sequence lengths.  Test infrastructure only.
+    for sampled checks at full sequence lengths.  ``kv_split`` > 1 emulates the kernel's KV
+    splits for small problems: each query tile's plan is cut into ns = min(kv_split, n)
+    contiguous entry ranges [s*n//ns, (s+1)*n//ns), each run from m = -inf, l = 0 (so the
+    lazy max and the P quantization restart per range), then merged with weights
+    2^(m_s - M).  With pv="f64" the split changes nothing but rounding.  Test
+    infrastructure only.
     """
     lazy = LAZY_RESCALE.get(pv, 0.0)
     ql, qh, kl, kh, v = operands(q, k, v, cfg)
@@ -487,29 +492,52 @@ def mixed_precision_attention(q, k, v, cfg: Cfg, pv: str = "f64", q_tiles=None) 
     out = np.full((lq, v.shape[1]), np.nan)
     for qt in (range(_cdiv(lq, tm)) if q_tiles is None else q_tiles):
         q0, q1 = qt * tm, min(qt * tm + tm, lq)
-        m = np.full(q1 - q0, -np.inf)
-        l = np.zeros(q1 - q0)  # l0 = 0, attention.py:100
-        acc = np.zeros((q1 - q0, v.shape[1]))
-        for kt, hi in tile_plan(qt, lq, lk, cfg):
-            k0, k1 = kt * tn, min(kt * tn + tn, lk)
-            s = (qh if hi else ql)[q0:q1] @ (kh if hi else kl)[k0:k1].T
-            if cfg.causal and k1 - 1 > q0:  # attention.py:306
-                qi = np.arange(q0, q1)[:, None]
-                kj = np.arange(k0, k1)[None, :]
-                s = np.where(qi >= kj, s, -np.inf)
-            m_new = np.maximum(m, s.max(axis=1))
-            if lazy:
-                m_new = np.where(m_new > m + lazy, m_new, m)
-            alive = np.isfinite(m_new)
-            alpha = np.where(alive, np.exp2(np.where(alive, m - m_new, 0.0)), 1.0)
-            p = np.zeros_like(s)
-            ok = np.isfinite(s)
-            p[ok] = np.exp2((s - np.where(alive, m_new, 0.0)[:, None])[ok])
-            l = l * alpha + p.sum(axis=1)
-            acc = acc * alpha[:, None] + _quantize_p(p, pv) @ v[k0:k1]
-            m = m_new
+        plan = tile_plan(qt, lq, lk, cfg)
+        ns = max(1, min(kv_split, len(plan)))
+        parts = []
+        for s in range(ns):
+            parts.append(_tile_range(ql, qh, kl, kh, v, cfg, pv, lazy, q0, q1, lk,
+                                     plan[s * len(plan) // ns:(s + 1) * len(plan) // ns]))
+        if ns == 1:
+            m, l, acc = parts[0]
+        else:
+            mm = np.max(np.stack([p_[0] for p_ in parts]), axis=0)
+            l = np.zeros(q1 - q0)
+            acc = np.zeros((q1 - q0, v.shape[1]))
+            for m_s, l_s, a_s in parts:
+                ok = np.isfinite(m_s)
+                w = np.where(ok, np.exp2(np.where(ok, m_s - np.where(np.isfinite(mm), mm, 0.0), 0.0)), 0.0)
+                l = l + w * l_s
+                acc = acc + w[:, None] * a_s
         out[q0:q1] = acc / np.where(l > 0, l, 1.0)[:, None]
     return out
+
+
+def _tile_range(ql, qh, kl, kh, v, cfg, pv, lazy, q0, q1, lk, entries):
+    """Online softmax (attention.py:150-175) of query rows [q0, q1) over plan entries."""
+    tn = cfg.tile_n
+    m = np.full(q1 - q0, -np.inf)
+    l = np.zeros(q1 - q0)  # l0 = 0, attention.py:100
+    acc = np.zeros((q1 - q0, v.shape[1]))
+    for kt, hi in entries:
+        k0, k1 = kt * tn, min(kt * tn + tn, lk)
+        s = (qh if hi else ql)[q0:q1] @ (kh if hi else kl)[k0:k1].T
+        if cfg.causal and k1 - 1 > q0:  # attention.py:306
+            qi = np.arange(q0, q1)[:, None]
+            kj = np.arange(k0, k1)[None, :]
+            s = np.where(qi >= kj, s, -np.inf)
+        m_new = np.maximum(m, s.max(axis=1))
+        if lazy:
+            m_new = np.where(m_new > m + lazy, m_new, m)
+        alive = np.isfinite(m_new)
+        alpha = np.where(alive, np.exp2(np.where(alive, m - m_new, 0.0)), 1.0)
+        p = np.zeros_like(s)
+        ok = np.isfinite(s)
+        p[ok] = np.exp2((s - np.where(alive, m_new, 0.0)[:, None])[ok])
+        l = l * alpha + p.sum(axis=1)
+        acc = acc * alpha[:, None] + _quantize_p(p, pv) @ v[k0:k1]
+        m = m_new
+    return m, l, acc
 
 
 def reference_attention(q, k, v, causal=False) -> np.ndarray:

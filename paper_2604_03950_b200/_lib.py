@@ -36,7 +36,7 @@ class DmaQuantArgs(C.Structure):
         ("low_format", C.c_int32),
         ("high_format", C.c_int32),
         ("granularity", C.c_int32),
-        ("_pad", C.c_int32),
+        ("kv_split", C.c_int32),
         ("packed_low", C.c_void_p),
         ("scales_low", C.c_void_p),
         ("high_codes", C.c_void_p),
@@ -72,7 +72,7 @@ class DmaAttnArgs(C.Structure):
         ("high_format", C.c_int32),
         ("granularity", C.c_int32),
         ("pv_mode", C.c_int32),
-        ("_pad", C.c_int32),
+        ("kv_split", C.c_int32),
         ("prescale", C.c_double),
         ("workspace", C.c_void_p),
         ("workspace_bytes", C.c_size_t),
@@ -105,6 +105,10 @@ def lib():
         L.dma_last_launch_count.restype = C.c_int
         L.dma_attention_set_fused.restype = C.c_int
         L.dma_attention_set_fused.argtypes = [C.c_int]
+        L.dma_attention_set_kv_split.restype = C.c_int
+        L.dma_attention_set_kv_split.argtypes = [C.c_int]
+        L.dma_attention_kv_split.restype = C.c_int
+        L.dma_attention_kv_split.argtypes = [C.POINTER(DmaAttnArgs)]
         L.dma_quantize_workspace_bytes.restype = sz
         L.dma_quantize_workspace_bytes.argtypes = [C.POINTER(DmaQuantArgs)]
         L.dma_quantize_dual.argtypes = [C.POINTER(DmaQuantArgs), vp]
@@ -149,6 +153,7 @@ EXPORTED_SYMBOLS = (
     "dma_attention_quantize", "dma_attention_core", "dma_tile_plan", "dma_high_precision_fraction",
     "dma_selftest_mma", "dma_last_error", "dma_abi_version", "dma_last_launch_count",
     "dma_decode_workspace_bytes", "dma_decode_attention", "dma_attention_set_fused",
+    "dma_attention_set_kv_split", "dma_attention_kv_split",
 )
 
 

@@ -141,7 +141,7 @@ class DmaAttention:
             self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device="cuda")
         return self._ws
 
-    def prepare(self, q, k, v, out=None, out_dtype=None):
+    def prepare(self, q, k, v, out=None, out_dtype=None, kv_split=0):
         """Validate the operands and build the C-ABI arguments.  The library takes raw
         pointers without strides, so layout mismatches are errors here, not silent."""
         import torch
@@ -174,6 +174,7 @@ class DmaAttention:
             raise ValueError(f"out must be a contiguous {q.device} tensor of shape {(B, H, Lq, DV)}")
         code = _lib.DT_BF16 if out.dtype == torch.bfloat16 else _lib.DT_F32
         a = _args(self.cfg, q, k, v, out, B, H, KVH, Lq, Lk, D, DV, code)
+        a.kv_split = kv_split  # 0: the library's policy (set before the workspace query)
         rc = _lib.lib().dma_attention_supported(a)
         _lib.check(rc, "dma_attention")
         ws = self.workspace_for(a)
@@ -321,6 +322,8 @@ class DmaAttention:
         # shapes: per-call allocations freed through record_stream kept the caching allocator
         # growing and now and then stalled a call on cudaMalloc / cudaFree (17 ms -> 30-100 ms)
         (s_in, s_cmp, s_out), bufs, fwds, marked, _ = self._pipe_entry(q, k, v, out, chunk_kv_heads)
+        # the chunks take the whole problem's KV split count: bit-identical to one device call
+        n_split = kv_split_count(q.shape, k.shape, v.shape, self.cfg)
         # every stream starts after the caller's prior work and after all of the previous call
         for st in (s_in, s_cmp, s_out):
             st.wait_stream(cur)
@@ -344,7 +347,7 @@ class DmaAttention:
                 s_cmp.wait_event(ev_in)
                 if ev_out[j] is not None:
                     s_cmp.wait_event(ev_out[j])
-                a, _ = fwds[j].prepare(dq, dk, dv, out=do)
+                a, _ = fwds[j].prepare(dq, dk, dv, out=do, kv_split=n_split)
                 _lib.check(_lib.lib().dma_attention_fwd(a, _lib.stream_ptr(s_cmp)), "dma_attention")
                 ev_cmp[j] = torch.cuda.Event()
                 ev_cmp[j].record(s_cmp)
@@ -382,6 +385,33 @@ def dma_attention(q, k, v, cfg: AttentionConfig, out=None, out_dtype=None, strea
     while o.dim() > nd:
         o = o.squeeze(0)
     return o
+
+
+class _Shape:
+    """Stand-in operand for _args: shape only (no device memory)."""
+
+    def __init__(self, dtype):
+        self.dtype = dtype
+
+    def data_ptr(self):
+        return 0
+
+
+def kv_split_count(q_shape, k_shape, v_shape, cfg: AttentionConfig) -> int:
+    """KV splits dma_attention_fwd uses for these [B, H, L, D] shapes under the current
+    mode (``dma_attention_set_kv_split``; 1 = unsplit).  Small problems (fewer head pairs x
+    query tiles than SMs) cut each tile plan into ranges merged in the kernel; the oracle's
+    PV emulation takes the same count (``kv_split=``)."""
+    import torch
+
+    B, H, Lq, D = q_shape
+    _, KVH, Lk, _ = k_shape
+    x = _Shape(torch.bfloat16)
+    a = _args(cfg, x, x, x, None, B, H, KVH, Lq, Lk, D, v_shape[-1], _lib.DT_F32)
+    n = int(_lib.lib().dma_attention_kv_split(a))
+    if n < 1:
+        _lib.check(-1, "dma_attention_kv_split")
+    return n
 
 
 def mixed_precision_attention(q, k, v, cfg: AttentionConfig):

@@ -153,8 +153,40 @@ struct PPParams {
   int n_pairs;
   int pairs_per_qt;
   int head_major;
-  unsigned int* ticket;  // [0] next pair, [1] CTAs done (self-resetting)
+  unsigned int* ticket;  // [0] next work item, [1] CTAs done (self-resetting)
+  // KV splits (small problems: fewer pairs than SMs).  Work item k = pair k / n_split, split
+  // k % n_split: a contiguous range of the pair's plan entries (item_range).  A split writes
+  // its unnormalised O rows with (m, l) to `part`; kv_combine_kernel merges the splits
+  // (flash-decoding style) and stores O.  n_split = 1: one item per pair.
+  int n_split;
+  int n_items;               // n_pairs * n_split (ticket bound)
+  float* part;               // [n_bh][n_qt][n_split][128 rows][DV + 4] f32: O row, (m, l) per half
 };
+
+// Plan entries [e0, e1) of split s of a pair whose plan has n entries: ns = min(n_split, n)
+// splits (at least 1) of near-equal length; s >= ns is an empty item (skipped by every role).
+// ns = 1 is the unsplit path (a pair with an empty plan still writes its zero rows).
+struct ItemRange {
+  int e0, e1, ns;
+  bool skip;
+};
+template <bool SPLIT>
+__device__ __forceinline__ ItemRange item_range(const PPParams& q, const Plan& plan, int s) {
+  ItemRange r;
+  if (!SPLIT) {  // one item per pair: compile-time constants, the unsplit kernel is unchanged
+    r.e0 = 0;
+    r.e1 = plan.n;
+    r.ns = 1;
+    r.skip = false;
+    return r;
+  }
+  r.ns = q.n_split < plan.n ? q.n_split : plan.n;
+  if (r.ns < 1) r.ns = 1;
+  r.skip = s >= r.ns;
+  r.e0 = r.skip ? 0 : static_cast<int>(static_cast<int64_t>(s) * plan.n / r.ns);
+  r.e1 = r.skip ? 0 : static_cast<int>(static_cast<int64_t>(s + 1) * plan.n / r.ns);
+  return r;
+}
 
 // Fused phase 1 (FUSE instantiations, bf16 inputs, TOKEN granularity): warps 10 / 11 of
 // every CTA quantize K + V tiles / Q tiles of the raw inputs into the operand layouts
@@ -274,7 +306,8 @@ struct PPCfg {
   static constexpr int oSqK = oSfV + kNV * 512;               // [2 stream][kNS][kSqkBytes]
   static constexpr int oSfP = oSqK + 2 * kNS * kSqkBytes;     // 512
   static constexpr int oSch = oSfP + 512;                     // [kNSch] int
-  static constexpr int oRed = oSch + 64;                      // [2 parity][2 stream][2 half][128] f32 row maxima, then l
+  static constexpr int oRed = oSch + 128;                     // [2 parity][2 stream][2 half][128] f32 row maxima, then l
+  static constexpr int kItmSlot = 16;                         // sched[16 + warp]: a softmax warp's current item
   static constexpr int oBar = oRed + (kSplit == 2 ? 2 * 4096 : 0);
   static constexpr int kSmemBytes = oBar + 512 + 1024;
   // TMEM columns
@@ -372,7 +405,7 @@ __device__ __forceinline__ void store_orow(const AttnParams& p, int64_t orow, in
   }
 }
 
-template <int D, int DV, int LOW, bool FUSE>
+template <int D, int DV, int LOW, bool FUSE, bool SPLIT>
 __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_kernel(const __grid_constant__ AttnParams p,
                                                              const __grid_constant__ PPParams pp,
                                                              const __grid_constant__ FuseParams fz) {
@@ -534,7 +567,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       unsigned int tk = 0;
       if (lane == 0) tk = atomicAdd(pp.ticket, 1u);
       tk = __shfl_sync(0xffffffffu, tk, 0);
-      const int k = tk < static_cast<unsigned int>(pp.n_pairs) ? static_cast<int>(tk) : -1;
+      const int k = tk < static_cast<unsigned int>(pp.n_items) ? static_cast<int>(tk) : -1;
       if (lane == 0) {
         sched[ss] = k;
         ptx::mbar_arrive(sch_full + ss);  // release: the slot write is visible to waiters
@@ -542,10 +575,11 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       __syncwarp();
       if (k < 0) break;
       int bh[2], qt;
-      pair_coords(p, pp, k, bh[0], bh[1], qt);
+      pair_coords(p, pp, SPLIT ? k / pp.n_split : k, bh[0], bh[1], qt);
       Plan plan;
       plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
-      if (plan.n == 0) continue;
+      const ItemRange ir = item_range<SPLIT>(pp, plan, SPLIT ? k % pp.n_split : 0);
+      if (ir.e0 >= ir.e1) continue;
       const int ns = bh[1] >= 0 ? 2 : 1;
       const int mk[2] = {mat_k_of(p, bh[0]), ns == 2 ? mat_k_of(p, bh[1]) : -1};
       const bool shared_kv = ns == 2 && mk[0] == mk[1];
@@ -575,7 +609,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       }
       // ---- per tile: K (+SF +S_q^K) per distinct KV head, then V (+SF)
       const int nk = shared_kv ? 1 : ns;
-      for (int e = 0; e < plan.n; ++e) {
+      for (int e = ir.e0; e < ir.e1; ++e) {
         int t;
         bool hi;
         plan.entry(e, t, hi);
@@ -652,10 +686,11 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       if (lane == 0) ptx::mbar_arrive(sch_empty + ss);
       if (k < 0) break;
       int bh[2], qt;
-      pair_coords(p, pp, k, bh[0], bh[1], qt);
+      pair_coords(p, pp, SPLIT ? k / pp.n_split : k, bh[0], bh[1], qt);
       Plan plan;
       plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
-      if (plan.n == 0) continue;
+      const ItemRange ir = item_range<SPLIT>(pp, plan, SPLIT ? k % pp.n_split : 0);
+      if (ir.e0 >= ir.e1) continue;
       const int ns = bh[1] >= 0 ? 2 : 1;
       const bool shared_kv = ns == 2 && mat_k_of(p, bh[0]) == mat_k_of(p, bh[1]);
       const int qs = static_cast<int>(po % C::kNQ);
@@ -687,7 +722,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         };
         if (!kEarlySF) wait_s_free();
         const uint32_t oq = C::oQ + (qs * 2 + x) * C::kQStream;
-        if (e == 0) {
+        if (e == ir.e0) {
           const uint32_t osfq = C::oSfQ + (qs * 2 + x) * C::kSfQ;
           for (int j = 0; j < C::kChHi; ++j) ptx::wu::tc_cp_sf(tmem + C::tSfQ(x) + 4 * j, sf_desc(osfq + 512 * j));
           if (LOW != kLowHigh)
@@ -760,7 +795,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         TRACE(true, 2, 12 + x);
         if (x == ns - 1 || !shared_kv) ptx::wu::tc_commit(k_empty + kslt);  // last reader of this K slot
         ptx::wu::tc_commit(s_full + x);
-        if (e == plan.n - 1 && x == ns - 1) ptx::wu::tc_commit(q_empty + qs);  // Q slot free after these
+        if (e == ir.e1 - 1 && x == ns - 1) ptx::wu::tc_commit(q_empty + qs);  // Q slot free after these
         TRACE(true, 2, 28 + x);
         PROF_MARK(9);
       };
@@ -804,7 +839,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
             const uint64_t ad = dhp | ptx::desc_lo(paddr + 32 * kk, 16);
             const uint64_t bd = dh | ptx::desc_lo(vaddr + kk * 32 * rb, 16);
             const uint32_t id = ptx::idesc_bs(0, 0, 0, 1, 128, DV, 1, kk & 3, kk & 3);
-            ptx::wu::mma_mxf8f6f4(tmem + C::tO(x), ad, bd, id, tmem + C::tSfP, tmem + C::tSfV(x), !(e == 0 && kk == 0));
+            ptx::wu::mma_mxf8f6f4(tmem + C::tO(x), ad, bd, id, tmem + C::tSfP, tmem + C::tSfV(x), !(e == ir.e0 && kk == 0));
           }
         } else {
 #pragma unroll
@@ -812,7 +847,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
           const uint64_t bd = dh | ptx::desc_lo(vaddr + kk * 32 * rb, 16);
           const uint32_t id = ptx::idesc_bs(0, 0, 0, 1, 128, DV, 1, kk & 3, kk & 3);
           ptx::wu::mma_mxf8f6f4_ts(tmem + C::tO(x), tmem + C::tP(x) + 8 * kk, bd, id, tmem + C::tSfP,
-                                   tmem + C::tSfV(x), !(e == 0 && kk == 0));
+                                   tmem + C::tSfV(x), !(e == ir.e0 && kk == 0));
         }
         }
         PROF_MARK(8);
@@ -824,30 +859,30 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       };
 
       if (kSplitPV) {
-        for (int e = 0; e < plan.n; ++e) {
+        for (int e = ir.e0; e < ir.e1; ++e) {
           issue_qk(0, e);
           if (ns == 2) issue_qk(1, e);
         }
       } else {
-      issue_qk(0, 0);
-      if (ns == 2) issue_qk(1, 0);
+      issue_qk(0, ir.e0);
+      if (ns == 2) issue_qk(1, ir.e0);
       if (kPvLate) {
         // stream B's PV(e - 1) after QK_A(e + 1): the QK that gates the S hand-over is not
         // queued behind four PV MMAs (measured slower with one P buffer per stream; with
         // kPSmem the PV is off the softmax chain)
-        for (int e = 0; e < plan.n; ++e) {
-          if (e + 1 < plan.n) issue_qk(0, e + 1);
-          if (ns == 2 && e > 0) issue_pv(1, e - 1);
+        for (int e = ir.e0; e < ir.e1; ++e) {
+          if (e + 1 < ir.e1) issue_qk(0, e + 1);
+          if (ns == 2 && e > ir.e0) issue_pv(1, e - 1);
           issue_pv(0, e);
-          if (ns == 2 && e + 1 < plan.n) issue_qk(1, e + 1);
+          if (ns == 2 && e + 1 < ir.e1) issue_qk(1, e + 1);
         }
-        if (ns == 2) issue_pv(1, plan.n - 1);
+        if (ns == 2) issue_pv(1, ir.e1 - 1);
       } else {
-      for (int e = 0; e < plan.n; ++e) {
-        if (e + 1 < plan.n) issue_qk(0, e + 1);
+      for (int e = ir.e0; e < ir.e1; ++e) {
+        if (e + 1 < ir.e1) issue_qk(0, e + 1);
         issue_pv(0, e);
         if (ns == 2) {
-          if (e + 1 < plan.n) issue_qk(1, e + 1);
+          if (e + 1 < ir.e1) issue_qk(1, e + 1);
           issue_pv(1, e);
         }
       }
@@ -879,23 +914,24 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       if (lane == 0) ptx::mbar_arrive(sch_empty + ss);
       if (k < 0) break;
       int bh0, bh1, qt;
-      pair_coords(p, pp, k, bh0, bh1, qt);
+      pair_coords(p, pp, SPLIT ? k / pp.n_split : k, bh0, bh1, qt);
       Plan plan;
       plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
-      if (plan.n == 0) continue;
+      const ItemRange ir = item_range<SPLIT>(pp, plan, SPLIT ? k % pp.n_split : 0);
+      if (ir.e0 >= ir.e1) continue;
       const int ns = bh1 >= 0 ? 2 : 1;
       const bool shared_kv = ns == 2 && mat_k_of(p, bh0) == mat_k_of(p, bh1);
       const int nk = shared_kv ? 1 : ns;
       const uint32_t vc0 = vc;
-      vc += nk * plan.n;
+      vc += nk * (ir.e1 - ir.e0);
       if (x >= ns) continue;  // odd head count: stream B idles on this pair
       constexpr int rb = DV;  // fp8 V row bytes (MN-major)
       const uint64_t dh = static_cast<uint64_t>(ptx::desc_hi(8 * rb, swz_mode(rb))) << 32;
-      for (int e = 0; e < plan.n; ++e) {
+      for (int e = ir.e0; e < ir.e1; ++e) {
         ptx::mbar_wait(p_full + x, pvc & 1);
         ++pvc;
         ptx::tc_fence_after();
-        const uint32_t vpos = vc0 + nk * e + (shared_kv ? 0 : x);
+        const uint32_t vpos = vc0 + nk * (e - ir.e0) + (shared_kv ? 0 : x);
         const uint32_t vslt = vpos % C::kNV;
         ptx::mbar_wait(v_full + vslt, (vpos / C::kNV) & 1);
         ptx::tc_fence_after();
@@ -905,7 +941,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         for (int kk = 0; kk < C::kBN / 32; ++kk) {
           const uint64_t bd = dh | ptx::desc_lo(vaddr + kk * 32 * rb, 16);
           const uint32_t id = ptx::idesc_bs(0, 0, 0, 1, 128, DV, 1, kk & 3, kk & 3);
-          ptx::wu::mma_mxf8f6f4_ts(tO, tmem + C::tP(x) + 8 * kk, bd, id, tsfp, tsfv, !(e == 0 && kk == 0));
+          ptx::wu::mma_mxf8f6f4_ts(tO, tmem + C::tP(x) + 8 * kk, bd, id, tsfp, tsfv, !(e == ir.e0 && kk == 0));
         }
         ptx::wu::tc_commit(v_empty + vslt);
         if (!shared_kv) ptx::wu::tc_commit(v_empty + vslt);
@@ -956,11 +992,15 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       if (lane == 0) ptx::mbar_arrive(sch_empty + ss);
       if (k < 0) break;
       int bh[2], qt;
-      pair_coords(p, pp, k, bh[0], bh[1], qt);
+      pair_coords(p, pp, SPLIT ? k / pp.n_split : k, bh[0], bh[1], qt);
       const int my_bh = bh[x];
       Plan plan;
       plan.init(qt, p.lq, p.lk, C::kBM, C::kBN, p.diag_window, p.sink_window, p.causal != 0);
-      if (my_bh < 0) continue;  // odd head count: stream B idles on this pair
+      const ItemRange ir = item_range<SPLIT>(pp, plan, SPLIT ? k % pp.n_split : 0);
+      if (my_bh < 0 || ir.skip) continue;  // odd head count: stream B idles on this pair
+      // the item index is parked in shared memory for the epilogue (the softmax runs at its
+      // register limit: nothing extra may stay live across the tile loop)
+      if (SPLIT && lane == 0) sched[C::kItmSlot + warp] = k;
       const bool pair2 = bh[1] >= 0;
       const int q0 = qt * C::kBM;
       const int qrow = q0 + row;
@@ -970,7 +1010,9 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       float m_run = -INFINITY;
       float2 l2 = make_float2(0.f, 0.f);
 
-      for (int e = 0; e < plan.n; ++e, ++g) {
+      bool first_split_tile = true;
+      for (int e = ir.e0; e < ir.e1; ++e, ++g, first_split_tile = false) {
+        const bool first_tile = SPLIT ? first_split_tile : e == 0;
         int t;
         bool hi;
         plan.entry(e, t, hi);
@@ -980,7 +1022,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         PROF_MARK(9);
         ptx::mbar_wait(s_full + x, g & 1);
         ptx::tc_fence_after();
-        if (FUSE && e == 0 && qrow < p.lq) sq_q = ld_acquire_f32(p.qs_q + static_cast<int64_t>(my_bh) * p.lq_pad + qrow);
+        if (FUSE && first_tile && qrow < p.lq) sq_q = ld_acquire_f32(p.qs_q + static_cast<int64_t>(my_bh) * p.lq_pad + qrow);
         TRACE(tw, x, 1);
         PROF_MARK(0);
         // load the first half of this thread's columns, start the second, scale the first while it lands
@@ -1108,7 +1150,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         if (kPSmem) {
           // P buffer g & 1 was read by PV(g - 2) (this stream's tile count g)
           if (g >= 2) ptx::mbar_wait(o_done + 2 * x + (g & 1), ((g - 2) >> 1) & 1);
-        } else if (e > 0) {
+        } else if (!first_tile) {
           ptx::mbar_wait(o_done + x, (g - 1) & 1);
           ptx::tc_fence_after();
         }
@@ -1166,7 +1208,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
             }
           }
 #if DMA_PP_LATE_PV_WAIT
-          if (q4 == 1 && e > 0) {
+          if (q4 == 1 && !first_tile) {
             ptx::mbar_wait(o_done + x, (g - 1) & 1);
             ptx::tc_fence_after();
           }
@@ -1189,7 +1231,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         TRACE(tw, x, 5);
         l2 = __ffma2_rn(l2, make_float2(alpha, alpha), ls);
         PROF_MARK(6);
-        if (e > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+        if (!first_tile && __any_sync(0xffffffffu, alpha != 1.0f)) {
           // this thread's O columns *= alpha
           if (kPSmem) {  // O holds PV(g - 1) once it completes
             ptx::mbar_wait(o_done + 2 * x + ((g - 1) & 1), ((g - 1) >> 1) & 1);
@@ -1229,7 +1271,17 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         my_l += rl[(hh ^ 1) * 128 + row];
       }
       const float inv_l = 1.0f / (my_l > 0.f ? my_l : 1.0f);
-      if (plan.n > 0) {
+      if (SPLIT) __syncwarp();
+      const int k_me = SPLIT ? sched[C::kItmSlot + warp] : k;
+      int qt_me;
+      {
+        int b0, b1;
+        pair_coords(p, pp, SPLIT ? k_me / pp.n_split : k_me, b0, b1, qt_me);
+      }
+      const int s_me = SPLIT ? k_me % pp.n_split : 0;
+      const ItemRange ir_me = item_range<SPLIT>(pp, plan, s_me);
+      const bool any = ir_me.e1 > ir_me.e0;
+      if (any) {
         if (kPSmem)
           ptx::mbar_wait(o_done + 2 * x + ((g - 1) & 1), ((g - 1) >> 1) & 1);
         else
@@ -1238,19 +1290,37 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       }
       const uint32_t tO = tmem + C::tO(x) + lane_base + OC * hh;
       const int64_t orow = static_cast<int64_t>(my_bh) * p.lq + qrow;
+      constexpr int kPartW = DV + 4;  // floats per partial row: O, then (m, l) of each column half
+      const bool split = SPLIT && ir_me.ns > 1;
+      const int64_t pslot = SPLIT ? (static_cast<int64_t>(my_bh) * p.n_qt + qt_me) * pp.n_split : 0;
 #pragma unroll
       for (int c = 0; c < OC / 32; ++c) {
         uint32_t rr[32];
-        if (plan.n > 0) {
+        if (any) {
           ptx::tmem_ld32(tO + 32 * c, rr);
           ptx::tmem_ld_wait();
         } else {
 #pragma unroll
           for (int i2 = 0; i2 < 32; ++i2) rr[i2] = 0u;
         }
-        if (qrow < p.lq) store_orow<DV>(p, orow, (OC / 32) * hh + c, rr, inv_l);
+        if (split) {
+          // unnormalised O of this split (relative to 2^(kPShift - m_run), as l)
+          float4* dst = reinterpret_cast<float4*>(pp.part + ((pslot + s_me) * 128 + row) * kPartW + OC * hh + 32 * c);
+#pragma unroll
+          for (int i2 = 0; i2 < 8; ++i2)
+            dst[i2] = make_float4(__uint_as_float(rr[4 * i2]), __uint_as_float(rr[4 * i2 + 1]),
+                                  __uint_as_float(rr[4 * i2 + 2]), __uint_as_float(rr[4 * i2 + 3]));
+        } else if (qrow < p.lq) {
+          store_orow<DV>(p, orow, (OC / 32) * hh + c, rr, inv_l);
+        }
       }
       ptx::tc_fence_before();
+      if (split) {
+        // (m, l) of the split next to its O row; kv_combine_kernel merges the splits
+        float* me = pp.part + ((pslot + s_me) * 128 + row) * kPartW + DV + 2 * hh;
+        me[0] = m_run;
+        me[1] = my_l;
+      }
       PROF_MARK(8);
     }
     if (kTurns && x == 0) ptx::named_bar_sync(1, 256 * kSplit);  // consume B's last hand-over
@@ -1260,6 +1330,65 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == kMma) ptx::tmem_dealloc<512>(tmem);
+}
+
+// Merge of the KV splits (PPParams n_split > 1): one warp per query row, lane = 4 output
+// columns.  O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s with M = max_s m_s: the online
+// softmax state merge of attention.py:150-175 across plan ranges.  Row blocks whose plan
+// has a single range were written by the attention kernel directly.
+template <int DV>
+__global__ void __launch_bounds__(256) kv_combine_kernel(const __grid_constant__ AttnParams p, const float* __restrict__ part,
+                                                         int n_split) {
+  constexpr int kPartW = DV + 4, kLanes = DV / 4;
+  ptx::pdl_wait();  // the attention kernel's partials
+  const int rows_per_cta = 256 / kLanes;
+  const int64_t blk = blockIdx.x;  // (bh, qt, row group)
+  const int groups = 128 / rows_per_cta;
+  const int64_t bq = blk / groups;
+  const int qt = static_cast<int>(bq % p.n_qt);
+  const int64_t bh = bq / p.n_qt;
+  const int row = static_cast<int>(blk % groups) * rows_per_cta + threadIdx.x / kLanes;
+  const int c4 = (threadIdx.x % kLanes) * 4;
+  const int qrow = qt * 128 + row;
+  if (qrow >= p.lq) return;
+  Plan plan;
+  plan.init(qt, p.lq, p.lk, 128, 128, p.diag_window, p.sink_window, p.causal != 0);
+  int ns = n_split < plan.n ? n_split : plan.n;
+  if (ns <= 1) return;
+  const float* base = part + ((bq * n_split) * 128 + row) * kPartW;
+  const int64_t sstride = 128 * kPartW;
+  float ms[16], ls[16];
+  float mm = -INFINITY;
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    ms[s] = s < ns ? __ldcg(base + s * sstride + DV) : -INFINITY;
+    ls[s] = s < ns ? __ldcg(base + s * sstride + DV + 1) : 0.f;
+    mm = fmaxf(mm, ms[s]);
+  }
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float ll = 0.f;
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    if (s < ns) {
+      const float w = ms[s] == -INFINITY ? 0.f : exp2f(ms[s] - mm);
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(base + s * sstride + c4));
+      ll += w * ls[s];
+      acc.x += w * v.x;
+      acc.y += w * v.y;
+      acc.z += w * v.z;
+      acc.w += w * v.w;
+    }
+  }
+  const float inv = 1.0f / (ll > 0.f ? ll : 1.0f);
+  const int64_t o = (bh * p.lq + qrow) * DV + c4;
+  if (p.out_bf16) {
+    __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(p.o) + o);
+    dst[0] = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+    dst[1] = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+  } else {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.o) + o) =
+        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+  }
 }
 
 }  // namespace dma

@@ -133,10 +133,78 @@ struct Layout {
   // byte offsets
   size_t q_hi, q_lo, k_hi, k_lo, v_codes, v_bf16;  // large buffers
   size_t small_begin, sf_q_hi, sf_q_lo, sf_k_hi, sf_k_lo, sf_v, qs_q, qs_k, ticket, fuse_flags, small_end;
+  int kv_split;    // KV splits per pair (ping-pong kernel, small problems; 1 = off)
+  size_t kv_part;  // split partials (kv_split > 1)
   size_t absmax_q, absmax_k, total;
 };
 
 static size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int num_sms();
+
+// KV splits (attn_pp.cuh PPParams): with fewer head pairs x query tiles than SMs the
+// persistent kernel leaves SMs idle and the longest causal row walks its whole plan alone
+// (c1: 8 work items, the last one 8 key tiles).  Splitting each pair's plan into ns
+// ranges of >= 2 tiles fills the GPU; the splits are merged in the kernel.
+// dma_attention_set_kv_split / DMA_KV_SPLIT: -1 auto (default), 0 or 1 off, n >= 2 force n.
+static std::atomic<int> g_kvsplit{-2};
+static int kv_split_mode() {
+  int v = g_kvsplit.load(std::memory_order_relaxed);
+  if (v == -2) {
+    const char* e = getenv("DMA_KV_SPLIT");
+    v = (e && e[0]) ? atoi(e) : -1;
+    if (v < -1) v = -1;
+    g_kvsplit.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+static constexpr int kMaxKvSplit = 16;
+
+static int kv_split_for(const DmaAttnArgs* a, int64_t mq, int64_t lq_pad) {
+  const int mode = a->kv_split > 0 ? (a->kv_split == 1 ? 1 : a->kv_split) : kv_split_mode();
+  if (mode == 0 || mode == 1 || a->len_q <= 0 || a->len_k <= 0) return 1;
+  const int64_t n_qt = lq_pad / 128, ppq = (mq + 1) / 2, pairs = ppq * n_qt;
+  const int sms = num_sms();
+  if (mode < 0 && pairs > sms) return 1;  // the dynamic scheduler balances the work items
+  int64_t maxn = 0, total = 0;  // longest plan, pair steps over all pairs
+  for (int64_t qt = 0; qt < n_qt && qt < 4096; ++qt) {
+    Plan pl;
+    pl.init(qt, a->len_q, a->len_k, 128, 128, a->diag_window, a->sink_window, a->causal != 0);
+    maxn = pl.n > maxn ? pl.n : maxn;
+    total += pl.n;
+  }
+  total *= ppq;
+  if (maxn < 2) return 1;
+  if (mode >= 2) {
+    const int64_t n = mode < maxn ? mode : maxn;
+    return static_cast<int>(n < kMaxKvSplit ? n : kMaxKvSplit);
+  }
+  // cost in pair steps (~1.6 us each on B200): the longest item or the average load per SM,
+  // plus, when split, the merge launch (~1.5 steps) and the partial rows written by the
+  // attention kernel and read back by the merge (~2.5 MB per us, fitted).  Measured on B200
+  // (tools/ks_sweep.py): c1 14.5 -> 11.2 us, B1 H2 N4096 56.6 -> 30.0 us, B1 H4 N8192 108 -> 81 us.
+  const double step_us = 1.6, mb_per_us = 2.5;
+  auto cost = [&](int64_t n) {
+    const double longest = static_cast<double>((maxn + n - 1) / n);
+    const double avg = static_cast<double>(total) / sms;
+    double c = longest > avg ? longest : avg;
+    if (n > 1) {
+      const double part_mb = static_cast<double>(mq) * n_qt * n * 128.0 * (a->v_dim + 4) * 4.0 * 2.0 / 1e6;
+      c += 1.5 + part_mb / mb_per_us / step_us;
+    }
+    return c;
+  };
+  int64_t best = 1;
+  double best_c = cost(1);
+  for (int64_t n = 2; n <= maxn && n <= kMaxKvSplit; ++n) {
+    const double c = cost(n);
+    if (c < 0.9 * best_c) {  // a split must win clearly
+      best = n;
+      best_c = c;
+    }
+  }
+  return static_cast<int>(best);
+}
 
 static Layout plan_layout(const DmaAttnArgs* a) {
   Layout L{};
@@ -191,7 +259,9 @@ static Layout plan_layout(const DmaAttnArgs* a) {
   L.ticket = take(64);  // dynamic pair scheduler ticket (zeroed with the small region; self-resetting)
   // fused forward: per 128-row tile ready flags (Q, K, V) + the quantizer work counters
   L.fuse_flags = L.pp ? take((L.mq * (L.lq_pad / 128) + 2 * L.mk * (L.lk_pad / 128)) * 4 + 64) : 0;
+  L.kv_split = L.pp ? kv_split_for(a, L.mq, L.lq_pad) : 1;
   L.small_end = off;
+  L.kv_part = L.kv_split > 1 ? take(L.mq * (L.lq_pad / 128) * L.kv_split * 128 * (DV + 4) * 4) : 0;
   L.absmax_q = L.tensor_gran ? take(L.mq * 8) : 0;
   L.absmax_k = L.tensor_gran ? take(L.mk * 8) : 0;
   L.total = off + 256;  // base alignment slack
@@ -620,6 +690,10 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
     PPParams q{};
     q.pairs_per_qt = static_cast<int>((L.mq + 1) / 2);
     q.n_pairs = q.pairs_per_qt * p.n_qt;
+    q.n_split = L.kv_split;
+    DMA_CHECK_ARG(static_cast<int64_t>(q.n_pairs) * q.n_split < (int64_t(1) << 31), "too many work items");
+    q.n_items = q.n_pairs * q.n_split;
+    q.part = L.kv_split > 1 ? reinterpret_cast<float*>(ws + L.kv_part) : nullptr;
     const double kv_bytes = static_cast<double>(L.mk) * static_cast<double>(L.lk_pad) * (2.6 * static_cast<double>(D));
     q.head_major = kv_bytes > 48.0 * 1024 * 1024;  // K/V exceed ~L2/2: keep all CTAs on the same heads
     q.ticket = reinterpret_cast<unsigned int*>(ws + L.ticket);
@@ -653,6 +727,11 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
       rc = run_pp(p, q, static_cast<int>(D), static_cast<int>(DV), low, st);
     }
     if (rc == 0) ++g_launches;
+    if (rc == 0 && q.n_split > 1) {
+      // merge the KV splits' partial rows (kv_combine_kernel, PDL: its launch overlaps the tail)
+      rc = run_kv_combine(p, q.part, q.n_split, static_cast<int>(DV), st);
+      if (rc == 0) ++g_launches;
+    }
     return rc;
   }
   const int rc = run_attn(p, static_cast<int>(D), static_cast<int>(DV), low, L.pv_bf16, items, st);
@@ -730,6 +809,7 @@ int dma_attention_fwd(const DmaAttnArgs* a, void* stream) {
   DMA_CHECK_ARG(a->q && a->k && a->v && a->o, "null tensor pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (fused_eligible(a, L)) {
+    L.kv_split = 1;  // one kernel per call: no KV splits (their merge is a second launch)
     // one kernel: the ping-pong attention with phase 1 in warps 10 / 11 (attn_pp.cuh FUSE)
     uint8_t* ws = ws_base(a);
     DMA_CUDA_TRY(cudaMemsetAsync(ws + L.small_begin, 0, L.small_end - L.small_begin, st));
@@ -741,6 +821,18 @@ int dma_attention_fwd(const DmaAttnArgs* a, void* stream) {
 }
 
 int dma_last_launch_count(void) { return g_launches; }
+
+int dma_attention_set_kv_split(int mode) {
+  const int prev = kv_split_mode();
+  g_kvsplit.store(mode < -1 ? -1 : mode, std::memory_order_relaxed);
+  return prev;
+}
+
+int dma_attention_kv_split(const DmaAttnArgs* a) {
+  if (validate(a)) return -1;
+  const Layout L = plan_layout(a);
+  return fused_eligible(a, L) ? 1 : L.kv_split;  // the fused forward never splits
+}
 
 int dma_attention_set_fused(int on) {
   const int prev = fuse_enabled() ? 1 : 0;

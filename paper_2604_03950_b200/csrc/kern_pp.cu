@@ -5,7 +5,8 @@ namespace dma {
 
 int run_pp(const AttnParams& p, const PPParams& q, int D, int DV, int low, cudaStream_t st) {
   const FuseParams none{};
-  return run_pp_t<false>(p, q, none, D, DV, low, st);
+  if (q.n_split > 1) return run_pp_split(p, q, D, DV, low, st);
+  return run_pp_t<false, false>(p, q, none, D, DV, low, st);
 }
 
 }  // namespace dma

@@ -11,13 +11,13 @@
 
 namespace dma {
 
-template <int D, int DV, int LOW, bool FUSE>
+template <int D, int DV, int LOW, bool FUSE, bool SPLIT>
 static int launch_pp(const AttnParams& p, const PPParams& q, const FuseParams& fz, cudaStream_t st) {
   using C = PPCfg<D, DV, LOW>;
-  auto kern = dma_attn_pp_kernel<D, DV, LOW, FUSE>;
+  auto kern = dma_attn_pp_kernel<D, DV, LOW, FUSE, SPLIT>;
   static_assert(C::kSmemBytes <= 227 * 1024, "smem budget");
   DMA_SET_SMEM_ONCE(kern, C::kSmemBytes);
-  const int grid = q.n_pairs < num_sms() ? q.n_pairs : num_sms();
+  const int grid = q.n_items < num_sms() ? q.n_items : num_sms();
   // PDL: the prologue (barriers, TMEM, descriptor prefetch) overlaps phase 1's tail; the
   // kernel pdl_waits before its first read of phase-1 data (the fused kernel has no
   // producer kernel before it: the attribute is then a no-op)
@@ -26,18 +26,21 @@ static int launch_pp(const AttnParams& p, const PPParams& q, const FuseParams& f
   return 0;
 }
 
-template <int D, int DV, bool FUSE>
+template <int D, int DV, bool FUSE, bool SPLIT>
 static int dispatch_pp(const AttnParams& p, const PPParams& q, const FuseParams& fz, int low, cudaStream_t st) {
-  if (low == kLowNV) return launch_pp<D, DV, kLowNV, FUSE>(p, q, fz, st);
-  if (low == kLowMX4) return launch_pp<D, DV, kLowMX4, FUSE>(p, q, fz, st);
-  return launch_pp<D, DV, kLowHigh, FUSE>(p, q, fz, st);
+  if (low == kLowNV) return launch_pp<D, DV, kLowNV, FUSE, SPLIT>(p, q, fz, st);
+  if (low == kLowMX4) return launch_pp<D, DV, kLowMX4, FUSE, SPLIT>(p, q, fz, st);
+  return launch_pp<D, DV, kLowHigh, FUSE, SPLIT>(p, q, fz, st);
 }
 
-template <bool FUSE>
+// SPLIT: the KV-split instantiation (PPParams n_split > 1, small problems); the unsplit
+// kernels carry none of its state (the softmax runs at its register limit)
+template <bool FUSE, bool SPLIT>
 static int run_pp_t(const AttnParams& p, const PPParams& q, const FuseParams& fz, int D, int DV, int low,
                     cudaStream_t st) {
-  if (D == 64) return DV == 64 ? dispatch_pp<64, 64, FUSE>(p, q, fz, low, st) : dispatch_pp<64, 128, FUSE>(p, q, fz, low, st);
-  return DV == 64 ? dispatch_pp<128, 64, FUSE>(p, q, fz, low, st) : dispatch_pp<128, 128, FUSE>(p, q, fz, low, st);
+  if (D == 64)
+    return DV == 64 ? dispatch_pp<64, 64, FUSE, SPLIT>(p, q, fz, low, st) : dispatch_pp<64, 128, FUSE, SPLIT>(p, q, fz, low, st);
+  return DV == 64 ? dispatch_pp<128, 64, FUSE, SPLIT>(p, q, fz, low, st) : dispatch_pp<128, 128, FUSE, SPLIT>(p, q, fz, low, st);
 }
 
 }  // namespace dma

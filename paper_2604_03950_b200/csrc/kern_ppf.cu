@@ -5,7 +5,8 @@
 namespace dma {
 
 int run_pp_fused(const AttnParams& p, const PPParams& q, const FuseParams& fz, int D, int DV, int low, cudaStream_t st) {
-  return run_pp_t<true>(p, q, fz, D, DV, low, st);
+  // the fused forward is one launch: never split (dma_attention_fwd forces n_split = 1)
+  return run_pp_t<true, false>(p, q, fz, D, DV, low, st);
 }
 
 }  // namespace dma

@@ -31,6 +31,8 @@ int num_sms();
 int run_attn(const AttnParams& p, int D, int DV, int low, bool pv_bf16, int64_t items, cudaStream_t st);
 int run_pp(const AttnParams& p, const PPParams& q, int D, int DV, int low, cudaStream_t st);
 int run_pp_fused(const AttnParams& p, const PPParams& q, const FuseParams& fz, int D, int DV, int low, cudaStream_t st);
+int run_pp_split(const AttnParams& p, const PPParams& q, int D, int DV, int low, cudaStream_t st);
+int run_kv_combine(const AttnParams& p, const float* part, int n_split, int DV, cudaStream_t st);
 int run_sk(const AttnParams& p, const SKParams& q, int D, int DV, int low, cudaStream_t st);
 int run_ws(const AttnParams& p, const SKParams& q, int D, int DV, int low, cudaStream_t st);
 }  // namespace dma

@@ -33,3 +33,13 @@ def record_parity(case, pv, rel, mx, erel=None, emx=None, **extra):
            "rel_l2_vs_emulation": erel, "max_abs_vs_emulation": emx, **extra}
     with open(os.path.join(d, f"parity_{os.getpid()}.jsonl"), "a") as f:
         f.write(json.dumps(row) + "\n")
+
+
+def kv_split_of(cfg, lq, lk, d, dv, B=1, H=1, KVH=1):
+    """The KV split count the forward uses for this problem (1 = unsplit): small problems
+    cut each query tile's plan into ranges merged in the kernel, and the oracle's PV
+    emulation must restart its lazy max / P quantization at the same range boundaries
+    (mx_oracle.mixed_precision_attention(..., kv_split=n))."""
+    import paper_2604_03950_b200 as m
+
+    return m.attention.kv_split_count((B, H, lq, d), (B, KVH, lk, d), (B, KVH, lk, dv), cfg)

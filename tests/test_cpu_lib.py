@@ -138,3 +138,25 @@ def test_attention_abi_validation_on_host():
                    (dict(diag_window=100), _lib.DMA_EINVAL)):
         assert L.dma_attention_supported(args(**kw)) == rc, kw
         assert L.dma_last_error()
+
+
+def test_kv_split_policy_host_only():
+    """dma_attention_kv_split / dma_attention_set_kv_split are host logic (no GPU needed):
+    small problems split, c3 does not, the per-call field and the global mode override."""
+    import paper_2604_03950_b200 as D
+    from paper_2604_03950_b200 import _lib
+
+    L = _lib.lib()
+    c = D.AttentionConfig(tile_m=128, tile_n=128, diag_window=128, sink_window=128, low_format=D.MXFP4)
+    ks = D.attention.kv_split_count
+    prev = L.dma_attention_set_kv_split(-1)
+    try:
+        assert ks((1, 1, 1024, 64), (1, 1, 1024, 64), (1, 1, 1024, 64), c) > 1
+        assert ks((1, 32, 32768, 128), (1, 32, 32768, 128), (1, 32, 32768, 128), c) == 1
+        L.dma_attention_set_kv_split(0)
+        assert ks((1, 1, 1024, 64), (1, 1, 1024, 64), (1, 1, 1024, 64), c) == 1
+        L.dma_attention_set_kv_split(3)
+        assert ks((1, 1, 1024, 64), (1, 1, 1024, 64), (1, 1, 1024, 64), c) == 3
+        assert ks((1, 1, 200, 64), (1, 1, 200, 64), (1, 1, 200, 64), c) == 2  # capped by the plan length
+    finally:
+        L.dma_attention_set_kv_split(prev)

@@ -20,7 +20,7 @@ import zlib
 import numpy as np
 import pytest
 
-from conftest import record_parity
+from conftest import kv_split_of, record_parity
 from inputs import randn_bf16
 from oracle import mx_oracle as O
 
@@ -85,7 +85,7 @@ def test_attention_vs_oracle(case, pv):
     got = D().mixed_precision_attention(q, k, v, c)
     want = O.mixed_precision_attention(q, k, v, oc)
     assert got.shape == want.shape and got.dtype == np.float64
-    emu = O.mixed_precision_attention(q, k, v, oc, pv=pv)
+    emu = O.mixed_precision_attention(q, k, v, oc, pv=pv, kv_split=kv_split_of(c, lq, lk, d, d))
     rel, mx = errs(got, want)
     erel, emx = errs(got, emu)
     print(f"{name} pv={pv}: vs oracle rel_l2={rel:.3e} max_abs={mx:.3e}; "
@@ -272,7 +272,7 @@ def test_attention_value_dim_differs(d, dv, low, causal, pv):
     got = D().mixed_precision_attention(q, k, v, c)
     assert got.shape == (lq, dv)
     want = O.mixed_precision_attention(q, k, v, oc)
-    emu = O.mixed_precision_attention(q, k, v, oc, pv=pv)
+    emu = O.mixed_precision_attention(q, k, v, oc, pv=pv, kv_split=kv_split_of(c, lq, lk, d, dv))
     rel, mx = errs(got, want)
     erel, emx = errs(got, emu)
     record_parity(f"dv_{d}_{dv}_{low}_{int(causal)}", pv, rel, mx, erel, emx)
@@ -319,7 +319,8 @@ def test_full_length_c3_sampled_tiles(pv):
                               out_dtype=torch.float32)[0].double().cpu().numpy()
     tiles = [0, 1, 97, 255]
     for h in range(H):
-        want = O.mixed_precision_attention(q[h], k[h], v[h], oc, pv=pv, q_tiles=tiles)
+        want = O.mixed_precision_attention(q[h], k[h], v[h], oc, pv=pv, q_tiles=tiles,
+                                           kv_split=kv_split_of(c, N, N, d, d, H=H, KVH=H))
         for t in tiles:
             r = slice(128 * t, 128 * t + 128)
             rel, mx = errs(got[h, r], want[r])
@@ -341,6 +342,7 @@ def test_float32_inputs_full_mantissa(pv):
                               out_dtype=torch.float32)[0].double().cpu().numpy()
     for h in range(H):
         want = O.mixed_precision_attention(q[h].astype(np.float64), k[h].astype(np.float64),
-                                           v[h].astype(np.float64), oc, pv=pv)
+                                           v[h].astype(np.float64), oc, pv=pv,
+                                           kv_split=kv_split_of(c, N, N, d, d, H=H, KVH=H))
         rel, mx = errs(got[h], want)
         assert rel <= TOL_EMU[pv][0] and mx <= TOL_EMU[pv][1], (pv, h, rel, mx)

@@ -16,7 +16,7 @@ Every case asserts against the oracle with the kernel's stated PV quantization
 import numpy as np
 import pytest
 
-from conftest import record_parity
+from conftest import kv_split_of, record_parity
 from inputs import randn_bf16
 from oracle import mx_oracle as O
 from test_gpu_attention import TOL, TOL_DEQ, TOL_DEQ_EMU, TOL_EMU, errs
@@ -41,10 +41,11 @@ def _cfgs(low, gran, T, S, pv):
     return c, oc
 
 
-def _check_tiles(name, pv, got_head, q, k, v, oc, tiles, tol, tol_emu):
-    """got_head [N, DV] (f64) vs the oracle (pv f64 = the reference) and its PV emulation."""
+def _check_tiles(name, pv, got_head, q, k, v, oc, tiles, tol, tol_emu, kv_split=1):
+    """got_head [N, DV] (f64) vs the oracle (pv f64 = the reference) and its PV emulation
+    (with the forward's KV split count: small problems split each tile plan)."""
     want = O.mixed_precision_attention(q, k, v, oc, q_tiles=tiles)
-    emu = O.mixed_precision_attention(q, k, v, oc, pv=pv, q_tiles=tiles)
+    emu = O.mixed_precision_attention(q, k, v, oc, pv=pv, q_tiles=tiles, kv_split=kv_split)
     rows = np.concatenate([np.arange(128 * t, min(128 * t + 128, q.shape[0])) for t in tiles])
     rel, mx = errs(got_head[rows], want[rows])
     erel, emx = errs(got_head[rows], emu[rows])
@@ -87,8 +88,10 @@ def test_c4_window_granularity_sweep(T, gran):
     got = _D().DmaAttention(c)(*(torch.from_numpy(x)[None].cuda() for x in (q, k, v)),
                                out_dtype=torch.float32)[0].double().cpu().numpy()
     tol, tol_emu = (TOL_DEQ[pv], TOL_DEQ_EMU[pv]) if gran == "block" else (TOL[pv], TOL_EMU[pv])
+    ks = kv_split_of(c, N, N, d, d, H=H, KVH=H)
     for h in range(H):
-        _check_tiles(f"c4_T{T}_{gran}_h{h}", pv, got[h], q[h], k[h], v[h], oc, [0, 1, 17, 64, 127], tol, tol_emu)
+        _check_tiles(f"c4_T{T}_{gran}_h{h}", pv, got[h], q[h], k[h], v[h], oc, [0, 1, 17, 64, 127], tol, tol_emu,
+                     kv_split=ks)
 
 
 @pytest.mark.parametrize("pv", ["mxfp8", "bf16"])

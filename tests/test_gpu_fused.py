@@ -52,9 +52,15 @@ def test_fused_forward_equals_two_phase(case):
     finally:
         L.dma_attention_set_fused(prev)
     fused = out.clone()
-    _lib.check(L.dma_attention_quantize(a, sp), "quantize")
-    _lib.check(L.dma_attention_core(a, sp), "core")
-    torch.cuda.synchronize()
+    # the fused forward never splits the KV range (one launch); compare with the unsplit
+    # two-phase path (small cases would otherwise take the KV-split kernel + merge)
+    prev_ks = L.dma_attention_set_kv_split(0)
+    try:
+        _lib.check(L.dma_attention_quantize(a, sp), "quantize")
+        _lib.check(L.dma_attention_core(a, sp), "core")
+        torch.cuda.synchronize()
+    finally:
+        L.dma_attention_set_kv_split(prev_ks)
     assert torch.isfinite(fused).all()
     assert torch.equal(fused, out), float((fused - out).abs().max())
 

@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 import torch
 
+from conftest import kv_split_of
 from inputs import randn_bf16
 from oracle import mx_oracle as O
 
@@ -57,7 +58,7 @@ def test_prefill_fuzz(seed):
                  high_format=hi_o, granularity=gran)
     q, k, v = randn_bf16(seed, lq, d), randn_bf16(seed + 100, lk, d), randn_bf16(seed + 200, lk, dv)
     got = m.mixed_precision_attention(q, k, v, cfg)
-    want = O.mixed_precision_attention(q, k, v, ocfg, pv=pv)
+    want = O.mixed_precision_attention(q, k, v, ocfg, pv=pv, kv_split=kv_split_of(cfg, lq, lk, d, dv))
     tol = TOL_EMU[pv] if tile == 128 else TOL_TILE64[pv]
     err = np.abs(got - want)
     rel = float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30))
