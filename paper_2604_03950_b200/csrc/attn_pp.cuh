@@ -153,6 +153,7 @@ struct PPParams {
   int n_pairs;
   int pairs_per_qt;
   int head_major;
+  int group_pairs;       // head_major: head pairs per group (their K/V share L2), walked longest-first
   unsigned int* ticket;  // [0] next work item, [1] CTAs done (self-resetting)
   // KV splits (small problems: fewer pairs than SMs).  Work item k = pair k / n_split, split
   // k % n_split: a contiguous range of the pair's plan entries (item_range).  A split writes
@@ -323,8 +324,16 @@ __device__ __forceinline__ void pair_coords(const AttnParams& p, const PPParams&
                                             int& qt) {
   int r, hp;
   if (q.head_major) {
-    hp = k / p.n_qt;
-    r = k - hp * p.n_qt;
+    // groups of group_pairs head pairs (K/V of a group fit in L2 with the others' traffic);
+    // inside a group, query-tile rank major: the longest tiles of all its pairs go first, so
+    // a group's long items never start at the very end of the launch (tail)
+    const int gsz = q.group_pairs * p.n_qt;
+    const int grp = k / gsz;
+    const int kin = k - grp * gsz;
+    const int g0 = grp * q.group_pairs;
+    const int gn = q.pairs_per_qt - g0 < q.group_pairs ? q.pairs_per_qt - g0 : q.group_pairs;
+    r = kin / gn;
+    hp = g0 + (kin - r * gn);
   } else {
     r = k / q.pairs_per_qt;
     hp = k - r * q.pairs_per_qt;

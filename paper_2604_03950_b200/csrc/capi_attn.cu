@@ -433,6 +433,16 @@ static int attn_kernel_choice() {
   }
   return v;
 }
+// K/V megabytes per head-major group of head pairs (DMA_GROUP_MB; 0 = one pair per group)
+static double group_kv_mb() {
+  static double v = -1.0;
+  if (v < 0.0) {
+    const char* e = getenv("DMA_GROUP_MB");
+    v = (e && e[0]) ? atof(e) : 48.0;
+  }
+  return v;
+}
+
 static bool use_sk_kernel() { return attn_kernel_choice() == kKernSK; }
 static bool use_ws_kernel() { return attn_kernel_choice() == kKernWS; }
 // The fused forward (phase 1 inside the ping-pong kernel, attn_pp.cuh FUSE) covers the
@@ -696,6 +706,13 @@ int attention_core(const DmaAttnArgs* a, const Layout& L, uint8_t* ws, cudaStrea
     q.part = L.kv_split > 1 ? reinterpret_cast<float*>(ws + L.kv_part) : nullptr;
     const double kv_bytes = static_cast<double>(L.mk) * static_cast<double>(L.lk_pad) * (2.6 * static_cast<double>(D));
     q.head_major = kv_bytes > 48.0 * 1024 * 1024;  // K/V exceed ~L2/2: keep all CTAs on the same heads
+    {
+      // head pairs per group: as many as keep the group's K/V under ~48 MB (c3: 2, c4: 4, c5: 1)
+      const double per_pair = kv_bytes / static_cast<double>(q.pairs_per_qt);
+      int gp = static_cast<int>(group_kv_mb() * 1024.0 * 1024.0 / per_pair);
+      gp = gp < 1 ? 1 : (gp > q.pairs_per_qt ? q.pairs_per_qt : gp);
+      q.group_pairs = gp;
+    }
     q.ticket = reinterpret_cast<unsigned int*>(ws + L.ticket);
     int rc;
     if (fuse) {
