@@ -1324,9 +1324,10 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
         }
       }
       ptx::tc_fence_before();
-      if (split) {
-        // (m, l) of the split next to its O row; kv_combine_kernel merges the splits
-        float* me = pp.part + ((pslot + s_me) * 128 + row) * kPartW + DV + 2 * hh;
+      if (split && hh == 0) {
+        // (m, l) of the split next to its O row (the row's, shared by both column halves);
+        // kv_combine_kernel merges the splits
+        float* me = pp.part + ((pslot + s_me) * 128 + row) * kPartW + DV;
         me[0] = m_run;
         me[1] = my_l;
       }
@@ -1360,18 +1361,34 @@ __global__ void __launch_bounds__(256) kv_combine_kernel(const __grid_constant__
   const int c4 = (threadIdx.x % kLanes) * 4;
   const int qrow = qt * 128 + row;
   if (qrow >= p.lq) return;
-  Plan plan;
-  plan.init(qt, p.lq, p.lk, 128, 128, p.diag_window, p.sink_window, p.causal != 0);
-  int ns = n_split < plan.n ? n_split : plan.n;
-  if (ns <= 1) return;
   const float* base = part + ((bq * n_split) * 128 + row) * kPartW;
   const int64_t sstride = 128 * kPartW;
+  // (m, l) of every slot in one round of loads (issued before the plan arithmetic); slots
+  // past this tile's range count ns were not written by this launch and are masked once ns
+  // is known.  ns = 1: the attention kernel wrote O itself
   float ms[16], ls[16];
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    if (s < n_split) {
+      const float4 h = __ldcg(reinterpret_cast<const float4*>(base + s * sstride + DV));
+      ms[s] = h.x;
+      ls[s] = h.y;
+    } else {
+      ms[s] = -INFINITY;
+      ls[s] = 0.f;
+    }
+  }
+  Plan plan;
+  plan.init(qt, p.lq, p.lk, 128, 128, p.diag_window, p.sink_window, p.causal != 0);
+  const int ns = n_split < plan.n ? n_split : plan.n;
+  if (ns <= 1) return;
   float mm = -INFINITY;
 #pragma unroll
   for (int s = 0; s < 16; ++s) {
-    ms[s] = s < ns ? __ldcg(base + s * sstride + DV) : -INFINITY;
-    ls[s] = s < ns ? __ldcg(base + s * sstride + DV + 1) : 0.f;
+    if (s >= ns) {
+      ms[s] = -INFINITY;
+      ls[s] = 0.f;
+    }
     mm = fmaxf(mm, ms[s]);
   }
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);

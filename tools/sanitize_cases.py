@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Small-shape runs of every libdma kernel family for compute-sanitizer (racecheck /
-synccheck / memcheck): quantize_dual, the ping-pong attention (two-phase and fused), the
+synccheck / memcheck): quantize_dual, the ping-pong attention (two-phase, KV-split and fused), the
 single-stream attention (bf16 PV and the BLOCK bf16-operand route) and the decode kernel."""
 import os
 import sys
@@ -23,9 +23,14 @@ x = x.clamp(-168 / 32.0, 168 / 32.0).to(torch.bfloat16)
 for low in (D.NVFP4, D.MXFP4):
     D.quantize_dual(x, False, low, D.MXFP8_E4M3)
 print("quantize ok")
+L = _lib.lib()
+ks = L.dma_attention_set_kv_split(0)
 D.dma_attention(q, k, v, D.AttentionConfig(**base))  # ping-pong kernel, two-phase
 print("pp ok")
-L = _lib.lib()
+L.dma_attention_set_kv_split(3)
+D.dma_attention(q, k, v, D.AttentionConfig(**base))  # KV-split ping-pong kernel + merge
+L.dma_attention_set_kv_split(ks)
+print("kv-split ok")
 prev = L.dma_attention_set_fused(1)
 D.dma_attention(q, k, v, D.AttentionConfig(**base))  # fused kernel
 L.dma_attention_set_fused(prev)
