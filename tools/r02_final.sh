@@ -19,6 +19,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:dma_
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r02_ncu_attn.log 2>&1; tail -1 gpurun_out/r02_ncu_attn.log
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:quant32 -s 2 -c 1 -o gpurun_out/r02_quant32_final -f \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r02_ncu_quant.log 2>&1; tail -1 gpurun_out/r02_ncu_quant.log
+timeout 300 python tools/ks_sweep.py > gpurun_out/r02_kvsplit_sweep.txt 2>&1; tail -4 gpurun_out/r02_kvsplit_sweep.txt
 for tool in racecheck synccheck memcheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_cases.py > gpurun_out/r02_sanitizer_$tool.log 2>&1
   echo "$tool rc=$?"; tail -2 gpurun_out/r02_sanitizer_$tool.log
