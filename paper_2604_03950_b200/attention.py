@@ -198,10 +198,10 @@ class DmaAttention:
         if bad:
             raise ValueError(_NONFINITE_MSG)
 
-    def __call__(self, q, k, v, out=None, out_dtype=None, stream=None):
+    def __call__(self, q, k, v, out=None, out_dtype=None, stream=None, kv_split=0):
         if not q.is_cuda:
             return self.forward_host(q, k, v, out=out, out_dtype=out_dtype)
-        a, out = self.prepare(q, k, v, out, out_dtype)
+        a, out = self.prepare(q, k, v, out, out_dtype, kv_split=kv_split)
         _lib.check(_lib.lib().dma_attention_fwd(a, _lib.stream_ptr(stream)), "dma_attention")
         if self.validate:
             self._check_finite(q, k, stream)
@@ -365,11 +365,13 @@ class DmaAttention:
             cur.wait_stream(st)
 
 
-def dma_attention(q, k, v, cfg: AttentionConfig, out=None, out_dtype=None, stream=None, validate=True):
+def dma_attention(q, k, v, cfg: AttentionConfig, out=None, out_dtype=None, stream=None, validate=True, kv_split=0):
     """Batched forward on CUDA tensors [B, H, L, D] (also accepts [H, L, D] / [L, D]).
 
     Functional drop-in: any layout (made contiguous), K / V cast to Q's dtype, and by
-    default the reference's ValueError on non-finite Q / K (``validate``)."""
+    default the reference's ValueError on non-finite Q / K (``validate``).  ``kv_split``:
+    0 = the library's small-problem policy, else this many KV splits (1 = unsplit; a caller
+    running pieces of a larger problem passes that problem's ``kv_split_count``)."""
     nd = q.dim()
     if nd not in (2, 3, 4):
         raise ValueError("Q, K, V must be 2-D, 3-D or 4-D")
@@ -381,7 +383,7 @@ def dma_attention(q, k, v, cfg: AttentionConfig, out=None, out_dtype=None, strea
     if not (q.dtype == k.dtype == v.dtype):
         k, v = k.to(q.dtype), v.to(q.dtype)
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
-    o = DmaAttention(cfg, validate=validate)(q, k, v, out=out, out_dtype=out_dtype, stream=stream)
+    o = DmaAttention(cfg, validate=validate)(q, k, v, out=out, out_dtype=out_dtype, stream=stream, kv_split=kv_split)
     while o.dim() > nd:
         o = o.squeeze(0)
     return o

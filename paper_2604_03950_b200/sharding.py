@@ -93,10 +93,17 @@ def dma_attention_sharded(q, k, v, cfg, group=None, compute=None, gather_output=
     """
     import torch.distributed as dist
 
-    if compute is None:
-        from .attention import dma_attention as compute
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if compute is None:
+        from .attention import dma_attention, kv_split_count
+
+        # every rank takes the whole problem's KV split count (small problems): the gathered
+        # O is then bit-identical to one device call over the whole problem at any world size
+        n_split = kv_split_count(q.shape, k.shape, v.shape, cfg)
+
+        def compute(ql, kl, vl, c):
+            return dma_attention(ql, kl, vl, c, kv_split=n_split)
     B, H = q.shape[0], q.shape[1]
     shard = plan_shard(B, H, k.shape[1], world, rank)
     ql, kl, vl = local_inputs(q, k, v, shard)

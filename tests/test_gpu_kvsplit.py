@@ -124,3 +124,29 @@ def test_split_is_deterministic_and_bf16_out(lib):
     lib.dma_attention_set_kv_split(0)
     z = D.dma_attention(q, k, v, c)
     assert float((x.float() - z.float()).abs().max()) < 0.05  # split vs unsplit: P-rounding only
+
+
+def test_pieces_with_whole_problem_count_are_bit_identical(lib):
+    """A caller that runs a small problem in (b, kv-head) pieces (sharding.py, the host
+    pipeline) passes the whole problem's split count: the pieces reproduce one call."""
+    import torch
+
+    import paper_2604_03950_b200 as D
+
+    c, _ = cfgs("nvfp4", "e4m3", "token", 128, 128, True, "mxfp8")
+    g = torch.Generator().manual_seed(17)
+    B, H, KVH, N, d = 2, 4, 2, 1024, 128
+    q = torch.randn(B, H, N, d, generator=g).to(torch.bfloat16).cuda()
+    k = torch.randn(B, KVH, N, d, generator=g).to(torch.bfloat16).cuda()
+    v = torch.randn(B, KVH, N, d, generator=g).to(torch.bfloat16).cuda()
+    lib.dma_attention_set_kv_split(4)  # (the policy leaves this shape unsplit)
+    n = D.attention.kv_split_count(q.shape, k.shape, v.shape, c)
+    assert n == 4
+    whole = D.dma_attention(q, k, v, c)
+    lib.dma_attention_set_kv_split(-1)  # the pieces alone would pick their own count
+    G = H // KVH
+    for b in range(B):
+        for kh in range(KVH):
+            piece = D.dma_attention(q[b:b + 1, kh * G:(kh + 1) * G], k[b:b + 1, kh:kh + 1], v[b:b + 1, kh:kh + 1], c,
+                                    kv_split=n)
+            assert torch.equal(piece, whole[b:b + 1, kh * G:(kh + 1) * G]), (b, kh)
