@@ -161,7 +161,7 @@ struct PPParams {
   // (flash-decoding style) and stores O.  n_split = 1: one item per pair.
   int n_split;
   int n_items;               // n_pairs * n_split (ticket bound)
-  float* part;               // [n_bh][n_qt][n_split][128 rows][DV + 4] f32: O row, (m, l) per half
+  float* part;               // [n_bh][n_qt][n_split][128 rows][DV + 4] f32: O row, (m, l), padding
 };
 
 // Plan entries [e0, e1) of split s of a pair whose plan has n entries: ns = min(n_split, n)
@@ -1299,7 +1299,7 @@ __global__ void __launch_bounds__(PPCfg<D, DV, LOW>::kThreads, 1) dma_attn_pp_ke
       }
       const uint32_t tO = tmem + C::tO(x) + lane_base + OC * hh;
       const int64_t orow = static_cast<int64_t>(my_bh) * p.lq + qrow;
-      constexpr int kPartW = DV + 4;  // floats per partial row: O, then (m, l) of each column half
+      constexpr int kPartW = DV + 4;  // floats per partial row: O, (m, l), 2 of padding (16-byte rows)
       const bool split = SPLIT && ir_me.ns > 1;
       const int64_t pslot = SPLIT ? (static_cast<int64_t>(my_bh) * p.n_qt + qt_me) * pp.n_split : 0;
 #pragma unroll
