@@ -30,7 +30,7 @@ class DmaAttnArgs(ctypes.Structure):  # include/dma.h: DmaAttnArgs (ABI 2)
                 ("v_dim", ctypes.c_int64), ("tile_m", ctypes.c_int32), ("tile_n", ctypes.c_int32),
                 ("diag_window", ctypes.c_int32), ("sink_window", ctypes.c_int32), ("causal", ctypes.c_int32),
                 ("low_format", ctypes.c_int32), ("high_format", ctypes.c_int32),
-                ("granularity", ctypes.c_int32), ("pv_mode", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("granularity", ctypes.c_int32), ("pv_mode", ctypes.c_int32), ("kv_split", ctypes.c_int32),
                 ("prescale", ctypes.c_double), ("workspace", ctypes.c_void_p),
                 ("workspace_bytes", ctypes.c_size_t), ("nonfinite", ctypes.c_void_p)]
 
